@@ -1,0 +1,160 @@
+/* eigenid_b200.h — C-ABI of the B200-native eigenvector–eigenvalue identity.
+ *
+ * This is the drop-in boundary for the reference hot path
+ * IdentityEngine::all_magnitudes (proj/src/identity.cpp:294-316) and the
+ * eigenvalue solver under it (proj/src/eigensolve.cpp:19-132).  The C++ host
+ * layer (include/eigenid/*.hpp, paper_2002_04989_b200/host/) and the Python
+ * mirror (paper_2002_04989_b200/engine.py) call only these entry points.
+ *
+ * Conventions
+ *  - All matrices are dense row-major FP64, symmetric; only the lower triangle
+ *    is read (the reference's build() guarantees exact symmetry,
+ *    proj/src/matrix.cpp:10-38).
+ *  - Output layout matches the reference: out[j*n + i] = |v_ij|^2, i the
+ *    ascending eigenvalue index, j the component (identity.cpp:311-313).
+ *  - Minor spectra mu are row-major, row j = ascending eigenvalues of M_j.
+ *  - Host-pointer entry points are synchronous and return an int status
+ *    (EIGENID_OK or an error code); `err` (nullable) receives the detail.
+ *    No exception ever crosses this boundary; the host layers re-throw the
+ *    matching eigenid::Error subclass (proj/include/eigenid/errors.hpp).
+ *  - *_device entry points take device pointers and a cudaStream_t (passed as
+ *    void*), enqueue work, and report errors at the next eigenid_gpu_sync().
+ *  - There is no CPU fallback: a missing device is EIGENID_E_DEVICE.
+ */
+#ifndef EIGENID_B200_H
+#define EIGENID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIGENID_B200_ABI_VERSION 1
+
+/* Status codes; 1..7 mirror the reference's typed errors. */
+enum eigenid_status {
+  EIGENID_OK = 0,
+  EIGENID_E_MATRIX_TOO_SMALL = 1, /* MatrixTooSmall        errors.hpp:31-34 */
+  EIGENID_E_DEGENERATE = 2,       /* DegenerateEigenvalue  errors.hpp:58-66 */
+  EIGENID_E_CONVERGENCE = 3,      /* ConvergenceFailure    errors.hpp:51-54 */
+  EIGENID_E_NONFINITE = 4,        /* NonFiniteIntermediate errors.hpp:69-72 */
+  EIGENID_E_INTERNAL = 5,         /* InternalInconsistency errors.hpp:74-77 */
+  EIGENID_E_CONFIG = 6,           /* ConfigError           errors.hpp:89-92 */
+  EIGENID_E_INDEX = 7,            /* IndexOutOfRange       errors.hpp:26-29 */
+  EIGENID_E_DEVICE = 20,          /* new: CUDA failure / no device          */
+  EIGENID_E_ALLOC = 21            /* new: device allocation failed          */
+};
+
+typedef struct eigenid_gpu_err {
+  int code;        /* eigenid_status */
+  int64_t index;   /* eigenvalue index (degeneracy) or matrix index; -1 */
+  double gap;      /* DegenerateEigenvalue::gap() */
+  int cuda_error;  /* cudaError_t when code == EIGENID_E_DEVICE */
+  char msg[256];
+} eigenid_gpu_err;
+
+/* Mirrors IdentityConfig (proj/include/eigenid/identity.hpp:81-93); the
+ * reference's `workers` has no device meaning and is absent. */
+typedef struct eigenid_gpu_config {
+  size_t batch_size;     /* >= 1, default 64 */
+  double degeneracy_tol; /* >= 0, default 1e-12, relative to spectral range */
+  int log_domain;        /* 1 = Evaluation::kLogDomain */
+} eigenid_gpu_config;
+
+typedef struct eigenid_gpu_ctx eigenid_gpu_ctx;
+
+/* Version of this ABI (EIGENID_B200_ABI_VERSION). */
+int eigenid_gpu_abi_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int eigenid_gpu_device_count(void);
+
+/* Context: device buffers and one stream, created once per engine like the
+ * reference's worker pool (identity.hpp:95-98, SPEC D5).  Calls on one
+ * context are serialised by an internal mutex (thread_pool.hpp:26-28). */
+int eigenid_gpu_create(eigenid_gpu_ctx** ctx, int device, eigenid_gpu_err* err);
+int eigenid_gpu_destroy(eigenid_gpu_ctx* ctx);
+void* eigenid_gpu_stream(eigenid_gpu_ctx* ctx); /* cudaStream_t */
+int eigenid_gpu_sync(eigenid_gpu_ctx* ctx, eigenid_gpu_err* err);
+
+/* ---- host-pointer entry points (reference-facing) ------------------- */
+
+/* Spectrum eigenvalues(const SymmetricMatrix&)   eigensolve.hpp:46,
+ * eigensolve.cpp:130-132.  out: n ascending eigenvalues. */
+int eigenid_gpu_eigenvalues(eigenid_gpu_ctx* ctx, const double* a, size_t n,
+                            double* out, eigenid_gpu_err* err);
+
+/* IdentityEngine::all_magnitudes   identity.hpp:133-135, identity.cpp:294-316.
+ * out: n*n, out[j*n+i].  lambda_out (n) / mu_out (n*(n-1)) nullable. */
+int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* ctx, const double* a, size_t n,
+                               const eigenid_gpu_config* cfg, double* out,
+                               double* lambda_out, double* mu_out,
+                               eigenid_gpu_err* err);
+
+/* Batched all_magnitudes over `count` independent n x n matrices stored
+ * back to back (a + t*n*n); out + t*n*n.  (SURVEY §8(b) addition, config C2.)
+ * On error, err->index is the first failing matrix. */
+int eigenid_gpu_all_magnitudes_batched(eigenid_gpu_ctx* ctx, const double* a,
+                                       size_t count, size_t n,
+                                       const eigenid_gpu_config* cfg,
+                                       double* out, eigenid_gpu_err* err);
+
+/* Minor spectra rows j0..j1-1 (and lambda(A)) — the n minor solves of
+ * identity.cpp:303-306.  mu: (j1-j0) x (n-1). lambda nullable. */
+int eigenid_gpu_minor_spectra(eigenid_gpu_ctx* ctx, const double* a, size_t n,
+                              size_t j0, size_t j1, double* lambda, double* mu,
+                              eigenid_gpu_err* err);
+
+/* Identity stage only (evaluate(), identity.cpp:185-238) from given spectra,
+ * rows j0..j1-1.  mu: (j1-j0) x (n-1); out: (j1-j0) x n.  (config C5.) */
+int eigenid_gpu_identity(eigenid_gpu_ctx* ctx, const double* lambda,
+                         const double* mu, size_t n, size_t j0, size_t j1,
+                         const eigenid_gpu_config* cfg, double* out,
+                         eigenid_gpu_err* err);
+
+/* Reference-style per-call instrumentation: eigenvalue solves performed by
+ * this context (identity.hpp:137-144).  all_magnitudes adds n+1. */
+size_t eigenid_gpu_solve_count(eigenid_gpu_ctx* ctx);
+void eigenid_gpu_reset_solve_count(eigenid_gpu_ctx* ctx);
+
+/* ---- device-pointer entry points (inputs resident in HBM) ------------ */
+
+/* Full pipeline for minor rows j0..j1-1 of a device-resident A: computes
+ * lambda(A) (redundantly per shard) and the minor spectra, then the identity
+ * rows.  d_out: (j1-j0) x n.  d_lambda (n) / d_mu ((j1-j0) x (n-1))
+ * nullable.  This is the per-rank shard of the multi-GPU path. */
+int eigenid_gpu_all_magnitudes_device(eigenid_gpu_ctx* ctx, const double* d_a,
+                                      size_t n, size_t j0, size_t j1,
+                                      const eigenid_gpu_config* cfg,
+                                      double* d_out, double* d_lambda,
+                                      double* d_mu, eigenid_gpu_err* err);
+
+/* Batched small matrices, device pointers. */
+int eigenid_gpu_all_magnitudes_batched_device(eigenid_gpu_ctx* ctx,
+                                              const double* d_a, size_t count,
+                                              size_t n,
+                                              const eigenid_gpu_config* cfg,
+                                              double* d_out,
+                                              eigenid_gpu_err* err);
+
+/* Identity stage, device pointers (rows j0..j1-1; d_mu row r = minor j0+r). */
+int eigenid_gpu_identity_device(eigenid_gpu_ctx* ctx, const double* d_lambda,
+                                const double* d_mu, size_t n, size_t j0,
+                                size_t j1, const eigenid_gpu_config* cfg,
+                                double* d_out, eigenid_gpu_err* err);
+
+/* C5 synthetic interlacing spectra generated on the device;
+ * bit-identical to oracle's orc_c5_mu_row. d_mu: (j1-j0) x (n-1). */
+int eigenid_gpu_c5_mu_device(eigenid_gpu_ctx* ctx, uint64_t seed,
+                             const double* d_lambda, size_t n, size_t j0,
+                             size_t j1, double* d_mu, eigenid_gpu_err* err);
+
+/* Number of kernels this context has launched (instrumentation for the
+ * bench's gpu_launches field). */
+uint64_t eigenid_gpu_launch_count(eigenid_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EIGENID_B200_H */

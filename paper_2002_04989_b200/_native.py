@@ -1,0 +1,103 @@
+"""ctypes binding of the C-ABI (include/eigenid_b200.h).
+
+Loads the in-tree libeigenid_b200.so built by build.py.  A missing library or
+device raises immediately — the product never falls back to CPU code.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import errors
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libeigenid_b200.so")
+
+_dp = C.POINTER(C.c_double)
+
+
+class GpuErr(C.Structure):
+    _fields_ = [("code", C.c_int), ("index", C.c_int64), ("gap", C.c_double),
+                ("cuda_error", C.c_int), ("msg", C.c_char * 256)]
+
+
+class GpuConfig(C.Structure):
+    _fields_ = [("batch_size", C.c_size_t), ("degeneracy_tol", C.c_double),
+                ("log_domain", C.c_int)]
+
+
+# every symbol the header declares, with its signature
+SIGNATURES = {
+    "eigenid_gpu_abi_version": (C.c_int, []),
+    "eigenid_gpu_device_count": (C.c_int, []),
+    "eigenid_gpu_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(GpuErr)]),
+    "eigenid_gpu_destroy": (C.c_int, [C.c_void_p]),
+    "eigenid_gpu_stream": (C.c_void_p, [C.c_void_p]),
+    "eigenid_gpu_sync": (C.c_int, [C.c_void_p, C.POINTER(GpuErr)]),
+    "eigenid_gpu_eigenvalues": (C.c_int, [C.c_void_p, _dp, C.c_size_t, _dp,
+                                          C.POINTER(GpuErr)]),
+    "eigenid_gpu_all_magnitudes": (C.c_int, [C.c_void_p, _dp, C.c_size_t,
+                                             C.POINTER(GpuConfig), _dp, _dp, _dp,
+                                             C.POINTER(GpuErr)]),
+    "eigenid_gpu_all_magnitudes_batched": (C.c_int, [C.c_void_p, _dp, C.c_size_t,
+                                                     C.c_size_t, C.POINTER(GpuConfig),
+                                                     _dp, C.POINTER(GpuErr)]),
+    "eigenid_gpu_minor_spectra": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t,
+                                            C.c_size_t, _dp, _dp, C.POINTER(GpuErr)]),
+    "eigenid_gpu_identity": (C.c_int, [C.c_void_p, _dp, _dp, C.c_size_t, C.c_size_t,
+                                       C.c_size_t, C.POINTER(GpuConfig), _dp,
+                                       C.POINTER(GpuErr)]),
+    "eigenid_gpu_solve_count": (C.c_size_t, [C.c_void_p]),
+    "eigenid_gpu_reset_solve_count": (None, [C.c_void_p]),
+    "eigenid_gpu_all_magnitudes_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t,
+                                                    C.c_size_t, C.c_size_t,
+                                                    C.POINTER(GpuConfig), C.c_void_p,
+                                                    C.c_void_p, C.c_void_p,
+                                                    C.POINTER(GpuErr)]),
+    "eigenid_gpu_all_magnitudes_batched_device": (C.c_int, [C.c_void_p, C.c_void_p,
+                                                            C.c_size_t, C.c_size_t,
+                                                            C.POINTER(GpuConfig),
+                                                            C.c_void_p,
+                                                            C.POINTER(GpuErr)]),
+    "eigenid_gpu_identity_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_size_t, C.c_size_t, C.c_size_t,
+                                              C.POINTER(GpuConfig), C.c_void_p,
+                                              C.POINTER(GpuErr)]),
+    "eigenid_gpu_c5_mu_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p,
+                                           C.c_size_t, C.c_size_t, C.c_size_t,
+                                           C.c_void_p, C.POINTER(GpuErr)]),
+    "eigenid_gpu_launch_count": (C.c_uint64, [C.c_void_p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Loads the CUDA library (raises DeviceError if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise errors.DeviceError(
+                f"{path} is missing: run __graft_entry__.build() "
+                "(the B200 path has no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(st: int, err: GpuErr):
+    if st:
+        errors.raise_for(st, err.msg.decode(errors="replace"), err.gap,
+                         err.cuda_error)
+
+
+def dptr(a) -> _dp:
+    return a.ctypes.data_as(_dp)

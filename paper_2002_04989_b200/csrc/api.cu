@@ -1,0 +1,729 @@
+// api.cu — the extern "C" boundary (include/eigenid_b200.h) and the device
+// pipeline behind it.
+//
+// all_magnitudes (identity.cpp:294-316) becomes, per call:
+//   n <= 64 : one fused kernel (small.cu), one CTA per matrix;
+//   n  > 64 : stage 1 dense->band (band.cu) for A and every minor in the
+//             shard, stage 2 band->tridiagonal (bulge.cu), Sturm bisection of
+//             lambda(A) (bisect.cu, Gershgorin brackets), the degeneracy check
+//             (identity.cpp:141-149), bisection of the minors inside the
+//             interlacing brackets, then the identity kernel (identity.cu).
+// Everything is enqueued on the context's stream with no host round trip;
+// host-pointer entry points copy in/out around it and translate the device
+// status record into the reference's typed errors.  There is no CPU
+// fallback: without a device every entry point returns EIGENID_E_DEVICE.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/eigenid_b200.h"
+#include "common.cuh"
+
+namespace eigenid_b200 {
+// small.cu
+cudaError_t launch_small_all(const double* dA, size_t count, int n, int batch,
+                             double tol, int log_domain, double* dout,
+                             double* dlam, double* dmu, DevStatus* dstatus,
+                             cudaStream_t stream);
+// identity.cu
+int identity_nb(int n, int batch);
+cudaError_t launch_identity(const double* dlam, const double* dmu, int n,
+                            int rows, int batch, double* dden, double* drcp,
+                            double* dout, unsigned long long* dflag_count,
+                            long long* dflags, long long flag_cap,
+                            DevStatus* dstatus, int log_domain, cudaStream_t st,
+                            int* launches);
+cudaError_t launch_degeneracy(const double* dlam, int n, double tol,
+                              DevStatus* dstatus, cudaStream_t st,
+                              int* launches);
+cudaError_t launch_c5_mu(uint64_t seed, const double* dlam, int n, int j0,
+                         int rows, double* dmu, cudaStream_t st, int* launches);
+// band.cu
+struct Stage1Args {
+  const double* A;
+  int n;
+  const int* js;
+  int nsolves;
+  double* ws;
+  long long ws_stride;
+  int ldw;
+  double* band;
+  long long band_stride;
+};
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
+int stage1_band_ld();
+int stage1_bandwidth();
+// bulge.cu
+struct Stage2Args {
+  double* band;
+  long long band_stride;
+  const int* js;
+  int nsolves;
+  int n;
+  double* d;
+  double* e2;
+  double* ae;
+  long long de_stride;
+};
+cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st);
+// bisect.cu
+struct BisectArgs {
+  const double* d;
+  const double* e2;
+  const double* ae;
+  long long de_stride;
+  const int* js;
+  int nsolves;
+  int first_solve;
+  int n;
+  const double* lam;
+  double* out;
+  long long out_ld;
+  int split;
+};
+cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
+                          cudaStream_t st, int* launches);
+
+__global__ void init_status_kernel(DevStatus* st) {
+  st[0].code = 0;
+  st[0].index = -1;
+  st[0].gap = 0.0;
+  st[0].aux = -1;
+  st[1].code = 0;
+  st[1].index = -1;  // == ULLONG_MAX for the atomicMin in degeneracy_kernel
+  st[1].gap = 0.0;
+  st[1].aux = -1;
+}
+
+__global__ void solve_list_kernel(int* js, int j0, int count) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= count;
+       t += gridDim.x * blockDim.x)
+    js[t] = t == 0 ? -1 : j0 + t - 1;
+}
+
+}  // namespace eigenid_b200
+
+using namespace eigenid_b200;
+
+namespace {
+
+constexpr int kSmallMax = 64;
+constexpr int kLargeMax = 14000;  // bisection stages (d, e^2) in shared memory
+constexpr int kStage1Slots = 148;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct eigenid_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevStatus* dstatus = nullptr;
+  DevStatus* hstatus = nullptr;  // pinned
+  DevBuf bA, bOut, bLam, bMu, bDen, bRcp, bFlags, bFlagCount, bWs, bBand, bD,
+      bE2, bAe, bJs, bTmpOut, bTmpMu;
+  std::atomic<size_t> solves{0};
+  std::atomic<uint64_t> launches{0};
+};
+
+namespace {
+
+void set_err(eigenid_gpu_err* err, int code, long long index, double gap,
+             int cuda_error, const std::string& msg) {
+  if (!err) return;
+  err->code = code;
+  err->index = index;
+  err->gap = gap;
+  err->cuda_error = cuda_error;
+  std::snprintf(err->msg, sizeof(err->msg), "%s", msg.c_str());
+}
+
+int cuda_fail(eigenid_gpu_err* err, cudaError_t e, const char* where) {
+  const int code = (e == cudaErrorMemoryAllocation) ? EIGENID_E_ALLOC
+                                                    : EIGENID_E_DEVICE;
+  set_err(err, code, -1, 0.0, (int)e,
+          std::string(where) + ": " + cudaGetErrorString(e));
+  return code;
+}
+
+#define EID_CUDA(call, where)                          \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(err, e_, where); \
+  } while (0)
+
+int check_cfg(const eigenid_gpu_config* cfg, eigenid_gpu_err* err) {
+  if (!cfg) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "null config");
+    return EIGENID_E_CONFIG;
+  }
+  if (cfg->batch_size < 1) {  // identity.cpp:126
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "batch size must be >= 1");
+    return EIGENID_E_CONFIG;
+  }
+  if (!(cfg->degeneracy_tol >= 0.0)) {  // identity.cpp:127-128
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0,
+            "degeneracy tolerance must be >= 0");
+    return EIGENID_E_CONFIG;
+  }
+  return EIGENID_OK;
+}
+
+int batch_of(const eigenid_gpu_config* cfg, int n) {
+  // batch sizes beyond n-1 behave like a single batch (prepare_batches)
+  return cfg->batch_size > (size_t)n ? n : (int)cfg->batch_size;
+}
+
+// Reads the device status (synchronising) and maps it to the C-ABI codes.
+int finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
+  EID_CUDA(cudaMemcpyAsync(c->hstatus, c->dstatus, 2 * sizeof(DevStatus),
+                           cudaMemcpyDeviceToHost, c->stream),
+           "status copy");
+  EID_CUDA(cudaStreamSynchronize(c->stream), "stream sync");
+  EID_CUDA(cudaGetLastError(), "kernel launch");
+  const DevStatus s = c->hstatus[0];
+  if (degenerate) *degenerate = false;
+  if (s.code == 0) return EIGENID_OK;
+  char buf[200];
+  switch (s.code) {
+    case EIGENID_E_DEGENERATE:
+      if (s.index >= 0 && s.aux < 0 && s.gap >= 0.0 && degenerate)
+        *degenerate = true;
+      if (s.aux >= 0)
+        std::snprintf(buf, sizeof buf,
+                      "spectrum is degenerate between eigenvalues %lld and %lld"
+                      " (matrix/row %lld)",
+                      s.index, s.index + 1, s.aux);
+      else
+        std::snprintf(buf, sizeof buf,
+                      "spectrum is degenerate between eigenvalues %lld and %lld",
+                      s.index, s.index + 1);
+      break;
+    case EIGENID_E_INTERNAL:
+      std::snprintf(buf, sizeof buf,
+                    "reconstructed squared magnitude is negative; eigenvalue "
+                    "ordering is inconsistent (i=%lld)", s.index);
+      break;
+    case EIGENID_E_CONVERGENCE:
+      std::snprintf(buf, sizeof buf, "eigenvalue solve did not converge");
+      break;
+    default:
+      std::snprintf(buf, sizeof buf, "device error code %d", s.code);
+  }
+  set_err(err, s.code, s.index, s.gap, 0, buf);
+  return s.code;
+}
+
+int begin(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
+  EID_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  init_status_kernel<<<1, 1, 0, c->stream>>>(c->dstatus);
+  EID_CUDA(cudaGetLastError(), "init_status");
+  c->launches += 1;
+  return EIGENID_OK;
+}
+
+// Large-n pipeline for minor rows [j0, j1) of a device matrix.
+int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
+              const eigenid_gpu_config* cfg, double* dout, double* dlam,
+              double* dmu, bool identity, eigenid_gpu_err* err) {
+  cudaStream_t st = c->stream;
+  const int rows = j1 - j0;
+  const int nsolves = 1 + rows;
+  const int kB = stage1_bandwidth();
+  const int ldab = stage1_band_ld();
+  const int ldw = (n + 7) & ~7;
+  const long long ws_stride = (long long)n * ldw + 3LL * n * kB;
+  const int slots = nsolves < kStage1Slots ? nsolves : kStage1Slots;
+  int launches = 0;
+  EID_CUDA(c->bJs.ensure(sizeof(int) * (size_t)nsolves), "alloc js");
+  EID_CUDA(c->bWs.ensure(sizeof(double) * (size_t)slots * ws_stride), "alloc ws");
+  const long long band_stride = (long long)n * ldab;
+  EID_CUDA(c->bBand.ensure(sizeof(double) * (size_t)nsolves * band_stride),
+           "alloc band");
+  EID_CUDA(c->bD.ensure(sizeof(double) * (size_t)nsolves * n), "alloc d");
+  EID_CUDA(c->bE2.ensure(sizeof(double) * (size_t)nsolves * n), "alloc e2");
+  EID_CUDA(c->bAe.ensure(sizeof(double) * (size_t)nsolves * n), "alloc ae");
+  int* djs = c->bJs.as<int>();
+  solve_list_kernel<<<(nsolves + 255) / 256, 256, 0, st>>>(djs, j0, rows);
+  ++launches;
+
+  Stage1Args s1{dA, n, djs, nsolves, c->bWs.as<double>(), ws_stride, ldw,
+                c->bBand.as<double>(), band_stride};
+  EID_CUDA(launch_stage1(s1, slots, st), "stage1");
+  ++launches;
+  Stage2Args s2{c->bBand.as<double>(), band_stride, djs, nsolves, n,
+                c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(), n};
+  EID_CUDA(launch_stage2(s2, st), "stage2");
+  ++launches;
+  // lambda(A): Gershgorin brackets, split across CTAs
+  BisectArgs ba{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
+                n, djs, nsolves, 0, n, nullptr, dlam, n, (n + 255) / 256};
+  EID_CUDA(launch_bisect(ba, 1, n, st, &launches), "bisect A");
+  if (identity) EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol,
+                                           c->dstatus, st, &launches),
+                         "degeneracy");
+  if (rows > 0) {
+    BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
+                  n, djs, nsolves, 1, n, dlam, dmu, n - 1, 1};
+    EID_CUDA(launch_bisect(bm, rows, n - 1, st, &launches), "bisect minors");
+  }
+  if (identity && rows > 0) {
+    const int batch = batch_of(cfg, n);
+    const int nb = identity_nb(n, batch);
+    EID_CUDA(c->bDen.ensure(sizeof(double) * (size_t)n * nb), "alloc den");
+    EID_CUDA(c->bRcp.ensure(sizeof(double) * (size_t)n * nb), "alloc rcp");
+    const long long cap = 1 << 20;
+    EID_CUDA(c->bFlags.ensure(sizeof(long long) * cap), "alloc flags");
+    EID_CUDA(c->bFlagCount.ensure(sizeof(unsigned long long)), "alloc flagc");
+    EID_CUDA(launch_identity(dlam, dmu, n, rows, batch, c->bDen.as<double>(),
+                             c->bRcp.as<double>(), dout,
+                             c->bFlagCount.as<unsigned long long>(),
+                             c->bFlags.as<long long>(), cap, c->dstatus,
+                             cfg->log_domain, st, &launches),
+             "identity");
+  }
+  c->launches += launches;
+  return EIGENID_OK;
+}
+
+// Full pipeline for rows [j0, j1) of a device matrix; dlam/dmu may be
+// null (scratch is used).
+int run_all(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
+            const eigenid_gpu_config* cfg, double* dout, double* dlam,
+            double* dmu, eigenid_gpu_err* err) {
+  const int rows = j1 - j0;
+  if (!dlam) {
+    EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+    dlam = c->bLam.as<double>();
+  }
+  if (n <= kSmallMax) {
+    const bool whole = (j0 == 0 && j1 == n);
+    double* o = dout;
+    double* mu = dmu;
+    if (!whole) {
+      EID_CUDA(c->bTmpOut.ensure(sizeof(double) * (size_t)n * n), "alloc tmp");
+      EID_CUDA(c->bTmpMu.ensure(sizeof(double) * (size_t)n * (n - 1)), "alloc tmp");
+      o = c->bTmpOut.as<double>();
+      mu = c->bTmpMu.as<double>();
+    }
+    EID_CUDA(launch_small_all(dA, 1, n, batch_of(cfg, n), cfg->degeneracy_tol,
+                              cfg->log_domain, o, dlam, mu, c->dstatus,
+                              c->stream),
+             "small");
+    c->launches += 1;
+    if (!whole) {
+      EID_CUDA(cudaMemcpyAsync(dout, o + (size_t)j0 * n,
+                               sizeof(double) * (size_t)rows * n,
+                               cudaMemcpyDeviceToDevice, c->stream),
+               "row copy");
+      if (dmu)
+        EID_CUDA(cudaMemcpyAsync(dmu, mu + (size_t)j0 * (n - 1),
+                                 sizeof(double) * (size_t)rows * (n - 1),
+                                 cudaMemcpyDeviceToDevice, c->stream),
+                 "mu copy");
+    }
+    return EIGENID_OK;
+  }
+  if (!dmu) {
+    EID_CUDA(c->bMu.ensure(sizeof(double) * (size_t)rows * (n - 1)), "alloc mu");
+    dmu = c->bMu.as<double>();
+  }
+  return run_large(c, dA, n, j0, j1, cfg, dout, dlam, dmu, true, err);
+}
+
+int identity_impl(eigenid_gpu_ctx* c, const double* d_lambda,
+                  const double* d_mu, size_t n, size_t j0, size_t j1,
+                  const eigenid_gpu_config* cfg, double* d_out,
+                  eigenid_gpu_err* err);
+
+int check_n(size_t n, eigenid_gpu_err* err) {
+  if (n < 2) {  // identity.cpp:296-297
+    set_err(err, EIGENID_E_MATRIX_TOO_SMALL, -1, 0.0, 0,
+            "component magnitudes need n >= 2");
+    return EIGENID_E_MATRIX_TOO_SMALL;
+  }
+  if (n > (size_t)kLargeMax) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0,
+            "n exceeds the eigensolver's supported size (14000)");
+    return EIGENID_E_CONFIG;
+  }
+  return EIGENID_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int eigenid_gpu_abi_version(void) { return EIGENID_B200_ABI_VERSION; }
+
+int eigenid_gpu_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int eigenid_gpu_create(eigenid_gpu_ctx** out, int device, eigenid_gpu_err* err) {
+  if (!out) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "null ctx pointer");
+    return EIGENID_E_CONFIG;
+  }
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count <= device || device < 0) {
+    set_err(err, EIGENID_E_DEVICE, -1, 0.0, (int)e,
+            "no CUDA device available (the B200 path has no CPU fallback)");
+    return EIGENID_E_DEVICE;
+  }
+  auto* c = new (std::nothrow) eigenid_gpu_ctx();
+  if (!c) {
+    set_err(err, EIGENID_E_ALLOC, -1, 0.0, 0, "host allocation failed");
+    return EIGENID_E_ALLOC;
+  }
+  c->device = device;
+  if ((e = cudaSetDevice(device)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) !=
+          cudaSuccess ||
+      (e = cudaMalloc(&c->dstatus, 2 * sizeof(DevStatus))) != cudaSuccess ||
+      (e = cudaMallocHost(&c->hstatus, 2 * sizeof(DevStatus))) != cudaSuccess) {
+    delete c;
+    return cuda_fail(err, e, "context creation");
+  }
+  *out = c;
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_destroy(eigenid_gpu_ctx* c) {
+  if (!c) return EIGENID_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DevBuf* b : {&c->bA, &c->bOut, &c->bLam, &c->bMu, &c->bDen, &c->bRcp,
+                    &c->bFlags, &c->bFlagCount, &c->bWs, &c->bBand, &c->bD,
+                    &c->bE2, &c->bAe, &c->bJs, &c->bTmpOut, &c->bTmpMu})
+    b->release();
+  cudaFree(c->dstatus);
+  cudaFreeHost(c->hstatus);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return EIGENID_OK;
+}
+
+void* eigenid_gpu_stream(eigenid_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int eigenid_gpu_sync(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
+  std::lock_guard<std::mutex> g(c->mu);
+  return finish(c, err, nullptr);
+}
+
+size_t eigenid_gpu_solve_count(eigenid_gpu_ctx* c) { return c->solves.load(); }
+void eigenid_gpu_reset_solve_count(eigenid_gpu_ctx* c) { c->solves.store(0); }
+uint64_t eigenid_gpu_launch_count(eigenid_gpu_ctx* c) { return c->launches.load(); }
+
+int eigenid_gpu_eigenvalues(eigenid_gpu_ctx* c, const double* a, size_t n,
+                            double* out, eigenid_gpu_err* err) {
+  if (n < 1) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "matrix dimension must be >= 1");
+    return EIGENID_E_CONFIG;
+  }
+  if (n > (size_t)kLargeMax) return check_n(n, err);
+  std::lock_guard<std::mutex> g(c->mu);
+  c->solves += 1;
+  if (n == 1) {  // tridiagonalize + QL of a 1x1 is the entry itself
+    out[0] = a[0];
+    return EIGENID_OK;
+  }
+  int st = begin(c, err);
+  if (st) return st;
+  EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D A");
+  eigenid_gpu_config cfg{64, 0.0, 0};
+  st = run_large(c, c->bA.as<double>(), (int)n, 0, 0, &cfg, nullptr,
+                 c->bLam.as<double>(), nullptr, false, err);
+  if (st) return st;
+  EID_CUDA(cudaMemcpyAsync(out, c->bLam.p, sizeof(double) * n,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "D2H lambda");
+  return finish(c, err, nullptr);
+}
+
+int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
+                               const eigenid_gpu_config* cfg, double* out,
+                               double* lambda_out, double* mu_out,
+                               eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  const size_t nn = n * n;
+  EID_CUDA(c->bA.ensure(sizeof(double) * nn), "alloc A");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * nn), "alloc out");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(c->bMu.ensure(sizeof(double) * n * (n - 1)), "alloc mu");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * nn,
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D A");
+  st = run_all(c, c->bA.as<double>(), (int)n, 0, (int)n, cfg,
+               c->bOut.as<double>(), c->bLam.as<double>(), c->bMu.as<double>(),
+               err);
+  if (st) return st;
+  EID_CUDA(cudaMemcpyAsync(out, c->bOut.p, sizeof(double) * nn,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "D2H out");
+  if (lambda_out)
+    EID_CUDA(cudaMemcpyAsync(lambda_out, c->bLam.p, sizeof(double) * n,
+                             cudaMemcpyDeviceToHost, c->stream),
+             "D2H lambda");
+  if (mu_out)
+    EID_CUDA(cudaMemcpyAsync(mu_out, c->bMu.p, sizeof(double) * n * (n - 1),
+                             cudaMemcpyDeviceToHost, c->stream),
+             "D2H mu");
+  bool degenerate = false;
+  st = finish(c, err, &degenerate);
+  // identity.cpp:299-306: lambda(A) is solved, then the degeneracy check
+  // throws before the n minor solves.
+  c->solves += (st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1;
+  return st;
+}
+
+int eigenid_gpu_all_magnitudes_batched(eigenid_gpu_ctx* c, const double* a,
+                                       size_t count, size_t n,
+                                       const eigenid_gpu_config* cfg,
+                                       double* out, eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  if (count == 0) return EIGENID_OK;
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  const size_t tot = count * n * n;
+  EID_CUDA(c->bA.ensure(sizeof(double) * tot), "alloc A");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * tot), "alloc out");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * tot,
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D A");
+  if (n <= (size_t)kSmallMax) {
+    EID_CUDA(launch_small_all(c->bA.as<double>(), count, (int)n,
+                              batch_of(cfg, (int)n), cfg->degeneracy_tol,
+                              cfg->log_domain, c->bOut.as<double>(), nullptr,
+                              nullptr, c->dstatus, c->stream),
+             "small batched");
+    c->launches += 1;
+  } else {
+    EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+    EID_CUDA(c->bMu.ensure(sizeof(double) * n * (n - 1)), "alloc mu");
+    for (size_t t = 0; t < count; ++t) {
+      st = run_all(c, c->bA.as<double>() + t * n * n, (int)n, 0, (int)n, cfg,
+                   c->bOut.as<double>() + t * n * n, c->bLam.as<double>(),
+                   c->bMu.as<double>(), err);
+      if (st) return st;
+    }
+  }
+  EID_CUDA(cudaMemcpyAsync(out, c->bOut.p, sizeof(double) * tot,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "D2H out");
+  st = finish(c, err, nullptr);
+  if (st == EIGENID_OK) c->solves += count * (n + 1);
+  return st;
+}
+
+int eigenid_gpu_minor_spectra(eigenid_gpu_ctx* c, const double* a, size_t n,
+                              size_t j0, size_t j1, double* lambda, double* mu,
+                              eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if (j0 > j1 || j1 > n) {
+    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, "minor range out of bounds");
+    return EIGENID_E_INDEX;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  const size_t rows = j1 - j0;
+  EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(c->bMu.ensure(sizeof(double) * (rows ? rows : 1) * (n - 1)), "alloc mu");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D A");
+  eigenid_gpu_config cfg{64, 0.0, 0};
+  st = run_large(c, c->bA.as<double>(), (int)n, (int)j0, (int)j1, &cfg, nullptr,
+                 c->bLam.as<double>(), c->bMu.as<double>(), false, err);
+  if (st) return st;
+  if (lambda)
+    EID_CUDA(cudaMemcpyAsync(lambda, c->bLam.p, sizeof(double) * n,
+                             cudaMemcpyDeviceToHost, c->stream),
+             "D2H lambda");
+  if (rows)
+    EID_CUDA(cudaMemcpyAsync(mu, c->bMu.p, sizeof(double) * rows * (n - 1),
+                             cudaMemcpyDeviceToHost, c->stream),
+             "D2H mu");
+  st = finish(c, err, nullptr);
+  if (st == EIGENID_OK) c->solves += 1 + rows;
+  return st;
+}
+
+int eigenid_gpu_identity(eigenid_gpu_ctx* c, const double* lambda,
+                         const double* mu, size_t n, size_t j0, size_t j1,
+                         const eigenid_gpu_config* cfg, double* out,
+                         eigenid_gpu_err* err) {
+  if (n < 2) return check_n(n, err);
+  int st = check_cfg(cfg, err);
+  if (st) return st;
+  if (j0 > j1 || j1 > n) {
+    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, "row range out of bounds");
+    return EIGENID_E_INDEX;
+  }
+  const size_t rows = j1 - j0;
+  if (rows == 0) return EIGENID_OK;
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(c->bMu.ensure(sizeof(double) * rows * (n - 1)), "alloc mu");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * rows * n), "alloc out");
+  EID_CUDA(cudaMemcpyAsync(c->bLam.p, lambda, sizeof(double) * n,
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D lambda");
+  EID_CUDA(cudaMemcpyAsync(c->bMu.p, mu, sizeof(double) * rows * (n - 1),
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D mu");
+  st = identity_impl(c, c->bLam.as<double>(), c->bMu.as<double>(), n, j0, j1,
+                     cfg, c->bOut.as<double>(), err);
+  if (st) return st;
+  EID_CUDA(cudaMemcpyAsync(out, c->bOut.p, sizeof(double) * rows * n,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "D2H out");
+  return finish(c, err, nullptr);
+}
+
+int eigenid_gpu_identity_device(eigenid_gpu_ctx* c, const double* d_lambda,
+                                const double* d_mu, size_t n, size_t j0,
+                                size_t j1, const eigenid_gpu_config* cfg,
+                                double* d_out, eigenid_gpu_err* err) {
+  if (n < 2) return check_n(n, err);
+  int st = check_cfg(cfg, err);
+  if (st) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  return identity_impl(c, d_lambda, d_mu, n, j0, j1, cfg, d_out, err);
+}
+
+}  // extern "C"
+
+namespace {
+int identity_impl(eigenid_gpu_ctx* c, const double* d_lambda,
+                  const double* d_mu, size_t n, size_t j0, size_t j1,
+                  const eigenid_gpu_config* cfg, double* d_out,
+                  eigenid_gpu_err* err) {
+  const int rows = (int)(j1 - j0);
+  if (rows <= 0) return EIGENID_OK;
+  int launches = 0;
+  const int batch = batch_of(cfg, (int)n);
+  const int nb = identity_nb((int)n, batch);
+  EID_CUDA(c->bDen.ensure(sizeof(double) * n * nb), "alloc den");
+  EID_CUDA(c->bRcp.ensure(sizeof(double) * n * nb), "alloc rcp");
+  const long long cap = 1 << 20;
+  EID_CUDA(c->bFlags.ensure(sizeof(long long) * cap), "alloc flags");
+  EID_CUDA(c->bFlagCount.ensure(sizeof(unsigned long long)), "alloc flagc");
+  EID_CUDA(launch_degeneracy(d_lambda, (int)n, cfg->degeneracy_tol, c->dstatus,
+                             c->stream, &launches),
+           "degeneracy");
+  EID_CUDA(launch_identity(d_lambda, d_mu, (int)n, rows, batch,
+                           c->bDen.as<double>(), c->bRcp.as<double>(), d_out,
+                           c->bFlagCount.as<unsigned long long>(),
+                           c->bFlags.as<long long>(), cap, c->dstatus,
+                           cfg->log_domain, c->stream, &launches),
+           "identity");
+  c->launches += launches;
+  return EIGENID_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int eigenid_gpu_all_magnitudes_device(eigenid_gpu_ctx* c, const double* d_a,
+                                      size_t n, size_t j0, size_t j1,
+                                      const eigenid_gpu_config* cfg,
+                                      double* d_out, double* d_lambda,
+                                      double* d_mu, eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  if (j0 > j1 || j1 > n) {
+    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, "row range out of bounds");
+    return EIGENID_E_INDEX;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  st = run_all(c, d_a, (int)n, (int)j0, (int)j1, cfg, d_out, d_lambda, d_mu, err);
+  if (st == EIGENID_OK) c->solves += 1 + (j1 - j0);
+  return st;
+}
+
+int eigenid_gpu_all_magnitudes_batched_device(eigenid_gpu_ctx* c,
+                                              const double* d_a, size_t count,
+                                              size_t n,
+                                              const eigenid_gpu_config* cfg,
+                                              double* d_out,
+                                              eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  if (n > (size_t)kSmallMax) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0,
+            "batched device entry supports n <= 64");
+    return EIGENID_E_CONFIG;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(launch_small_all(d_a, count, (int)n, batch_of(cfg, (int)n),
+                            cfg->degeneracy_tol, cfg->log_domain, d_out,
+                            nullptr, nullptr, c->dstatus, c->stream),
+           "small batched");
+  c->launches += 1;
+  c->solves += count * (n + 1);
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_c5_mu_device(eigenid_gpu_ctx* c, uint64_t seed,
+                             const double* d_lambda, size_t n, size_t j0,
+                             size_t j1, double* d_mu, eigenid_gpu_err* err) {
+  if (n < 2) return check_n(n, err);
+  std::lock_guard<std::mutex> g(c->mu);
+  int launches = 0;
+  EID_CUDA(launch_c5_mu(seed, d_lambda, (int)n, (int)j0, (int)(j1 - j0), d_mu,
+                        c->stream, &launches),
+           "c5 mu");
+  c->launches += launches;
+  return EIGENID_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// bisect.cu — K2: Sturm-count bisection for the tridiagonals of stage 2.
+//
+// Replaces the implicit-shift QL + std::sort of eigensolve.cpp:72-128.
+// Output is ascending by construction (a final check enforces the Spectrum
+// contract exactly).  For the minors the bracket of eigenvalue k is the
+// interlacing interval [lambda_k(A), lambda_{k+1}(A)] widened by the solver
+// error and verified by Sturm counts at both ends; if
+// either check fails the Gershgorin interval is used instead.
+// One CTA per minor stages (d, e^2) in shared memory (64 KB at m = 4095);
+// one thread per eigenvalue, so every Sturm step of a warp is a broadcast
+// shared-memory read.
+#include "common.cuh"
+
+namespace eigenid_b200 {
+
+constexpr int kBisNT = 256;
+
+struct BisectArgs {
+  const double* d;
+  const double* e2;
+  const double* ae;
+  long long de_stride;
+  const int* js;
+  int nsolves;
+  int first_solve;       // solve index of the first CTA (blockIdx.x offset)
+  int n;
+  const double* lam;     // interlacing brackets (nullptr: Gershgorin only)
+  double* out;           // row r = solve first_solve + r ... see out_ld
+  long long out_ld;
+  int split;             // CTAs per solve (eigenvalue ranges), >= 1
+};
+
+__device__ double block_reduce_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = red[0];
+  for (int w = 1; w < kBisNT / 32; ++w) t = fmax(t, red[w]);
+  __syncthreads();
+  return t;
+}
+__device__ double block_reduce_min(double v, double* red) {
+  return -block_reduce_max(-v, red);
+}
+
+__global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double red[kBisNT / 32];
+  __shared__ int unsorted;
+  const int solve = a.first_solve + blockIdx.x / a.split;
+  const int part = blockIdx.x % a.split;
+  const int m = a.js[solve] < 0 ? a.n : a.n - 1;
+  double* sd = sm;
+  double* se2 = sm + m;
+  const double* gd = a.d + solve * a.de_stride;
+  const double* ge2 = a.e2 + solve * a.de_stride;
+  const double* gae = a.ae + solve * a.de_stride;
+  double glo = 1e308, ghi = -1e308, tn = 0.0, emax = 0.0;
+  for (int k = threadIdx.x; k < m; k += kBisNT) {
+    const double dk = gd[k];
+    sd[k] = dk;
+    if (k + 1 < m) {
+      se2[k] = ge2[k];
+      emax = fmax(emax, ge2[k]);
+    }
+    const double r = (k > 0 ? gae[k - 1] : 0.0) + (k + 1 < m ? gae[k] : 0.0);
+    glo = fmin(glo, dk - r);
+    ghi = fmax(ghi, dk + r);
+    tn = fmax(tn, fabs(dk) + r);
+  }
+  glo = block_reduce_min(glo, red);
+  ghi = block_reduce_max(ghi, red);
+  tn = block_reduce_max(tn, red);
+  emax = block_reduce_max(emax, red);
+  const double pivmin = kSafeMin * fmax(1.0, emax);
+  const double fudge = 2.0 * kEps * tn * m + 2.0 * pivmin;
+  glo -= fudge;
+  ghi += fudge;
+  const double atol = kEps * tn;
+  const double delta = 8.0 * (m + 1) * kEps * tn + pivmin;
+  double* out = a.out + (long long)(solve - a.first_solve) * a.out_ld;
+  const int per = (m + a.split - 1) / a.split;
+  const int k0 = part * per, k1 = min(m, k0 + per);
+  for (int k = k0 + threadIdx.x; k < k1; k += kBisNT) {
+    double lo = glo, hi = ghi;
+    if (a.lam) {
+      const double l0 = a.lam[k] - delta, l1 = a.lam[k + 1] + delta;
+      if (sturm_count(sd, se2, m, l0, pivmin) <= k &&
+          sturm_count(sd, se2, m, l1, pivmin) > k) {
+        lo = fmax(l0, glo);
+        hi = fmin(l1, ghi);
+        if (!(lo < hi)) {
+          lo = glo;
+          hi = ghi;
+        }
+      }
+    }
+    out[k] = bisect_one(sd, se2, m, k, lo, hi, atol, pivmin);
+  }
+  if (a.split > 1) return;  // cross-CTA order is checked by sort_fix_kernel
+  __syncthreads();
+  if (threadIdx.x == 0) unsorted = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k + 1 < m; k += kBisNT)
+    if (out[k + 1] < out[k]) unsorted = 1;
+  __syncthreads();
+  if (unsorted && threadIdx.x == 0) {
+    for (int k = 1; k < m; ++k) {
+      const double v = out[k];
+      int t = k - 1;
+      while (t >= 0 && out[t] > v) {
+        out[t + 1] = out[t];
+        --t;
+      }
+      out[t + 1] = v;
+    }
+  }
+}
+
+// Enforces ascending order of one spectrum written by a split bisection.
+__global__ void sort_fix_kernel(double* out, int m) {
+  __shared__ int unsorted;
+  if (threadIdx.x == 0) unsorted = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k + 1 < m; k += blockDim.x)
+    if (out[k + 1] < out[k]) unsorted = 1;
+  __syncthreads();
+  if (unsorted && threadIdx.x == 0) {
+    for (int k = 1; k < m; ++k) {
+      const double v = out[k];
+      int t = k - 1;
+      while (t >= 0 && out[t] > v) {
+        out[t + 1] = out[t];
+        --t;
+      }
+      out[t + 1] = v;
+    }
+  }
+}
+
+cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
+                          cudaStream_t st, int* launches) {
+  const size_t smem = sizeof(double) * 2 * (size_t)mmax;
+  cudaError_t e = cudaFuncSetAttribute(
+      bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  bisect_kernel<<<nsolves_here * a.split, kBisNT, smem, st>>>(a);
+  ++*launches;
+  if (a.split > 1) {
+    for (int s = 0; s < nsolves_here; ++s) {
+      sort_fix_kernel<<<1, 256, 0, st>>>(a.out + s * a.out_ld, mmax);
+      ++*launches;
+    }
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace eigenid_b200

@@ -1,0 +1,159 @@
+// common.cuh — shared device helpers for the eigenid B200 kernels.
+//
+// Arithmetic that must round exactly like the reference (the identity
+// products, identity.cpp:206-225) uses the explicit __d*_rn intrinsics so
+// nvcc can never contract it into FMAs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eigenid_b200 {
+
+constexpr double kEps = 2.220446049250313080847e-16;   // DBL_EPSILON
+constexpr double kSafeMin = 2.2250738585072014e-308;   // DBL_MIN
+
+// Per-solve / per-call device status record (reduced with atomics).
+struct DevStatus {
+  int code;        // eigenid_status
+  int pad;
+  long long index; // eigenvalue index (degeneracy) / component index
+  double gap;
+  long long aux;   // matrix index (batched) or output row
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Records the first error of a call (lowest code wins ties deterministically
+// enough for reporting; any error aborts the call on the host side).
+__device__ __forceinline__ void set_status(DevStatus* st, int code,
+                                           long long index, double gap,
+                                           long long aux = -1) {
+  if (atomicCAS(&st->code, 0, code) == 0) {
+    st->index = index;
+    st->gap = gap;
+    st->aux = aux;
+  }
+}
+
+// Sturm count: number of eigenvalues of the symmetric tridiagonal (d, e2)
+// strictly below x (LAPACK dlaebz convention: a zero pivot is replaced by
+// -pivmin and counts as negative).  e2[k] = offdiag[k]^2, k = 0..m-2.
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d,
+                                           const double* __restrict__ e2,
+                                           int m, double x, double pivmin) {
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  for (int k = 1; k < m; ++k) {
+    q = (d[k] - x) - e2[k - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// Bisects eigenvalue k (0-based, ascending) of (d, e2) inside [lo, hi) with
+// count(lo) <= k < count(hi) already established.  Stops at
+// hi - lo <= max(atol, 2 eps max(|lo|,|hi|)) — the accuracy the
+// Householder reduction's backward error (~eps ||T||) supports.
+__device__ __forceinline__ double bisect_one(const double* __restrict__ d,
+                                             const double* __restrict__ e2,
+                                             int m, int k, double lo, double hi,
+                                             double atol, double pivmin) {
+  for (int it = 0; it < 200; ++it) {
+    const double w = hi - lo;
+    const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
+    if (w <= tol) break;
+    const double mid = lo + 0.5 * w;
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_count(d, e2, m, mid, pivmin) > k)
+      hi = mid;
+    else
+      lo = mid;
+  }
+  return lo + 0.5 * (hi - lo);
+}
+
+// One |v_ij|^2 exactly as evaluate() computes it (identity.cpp:185-238):
+// the sorted pairing equals the reversed natural order, so
+// sorted index s pairs lambda_i - mu[n-2-s] with lambda_i - lambda[k'],
+// k = n-2-s, k' = k + (k >= i); batches of `batch` pairs, ratio num/den per
+// batch, product of ratios in batch order.  Returns raw (pre-clamp); the
+// caller retries in the log domain when it is not finite.
+__device__ __forceinline__ double identity_batched(const double* __restrict__ lam,
+                                                   const double* __restrict__ mu,
+                                                   int n, int i, int batch) {
+  const double li = lam[i];
+  double raw = 1.0, num = 1.0, den = 1.0;
+  int cnt = 0;
+  for (int s = 0; s < n - 1; ++s) {
+    const int k = n - 2 - s;
+    const int kd = k + (k >= i);
+    num = __dmul_rn(num, __dsub_rn(li, mu[k]));
+    den = __dmul_rn(den, __dsub_rn(li, lam[kd]));
+    if (++cnt == batch || s == n - 2) {
+      raw = __dmul_rn(raw, __ddiv_rn(num, den));
+      num = 1.0;
+      den = 1.0;
+      cnt = 0;
+    }
+  }
+  return raw;
+}
+
+// log_domain_product over the sorted pairing (identity.cpp:98-122).
+// Returns 0 on success, 2 (zero denominator -> DegenerateEigenvalue) or
+// 5 (negative square -> InternalInconsistency).
+__device__ __forceinline__ int identity_log_domain(const double* __restrict__ lam,
+                                                   const double* __restrict__ mu,
+                                                   int n, int i, double* out) {
+  const double li = lam[i];
+  double log_sum = 0.0;
+  bool negative = false, zero = false;
+  for (int s = 0; s < n - 1; ++s) {
+    const double x = __dsub_rn(li, mu[n - 2 - s]);
+    if (x == 0.0) {
+      zero = true;
+    } else {
+      log_sum += log(fabs(x));
+      if (x < 0.0) negative = !negative;
+    }
+  }
+  for (int s = 0; s < n - 1; ++s) {
+    const int k = n - 2 - s;
+    const double x = __dsub_rn(li, lam[k + (k >= i)]);
+    if (x == 0.0) return 2;
+    log_sum -= log(fabs(x));
+    if (x < 0.0) negative = !negative;
+  }
+  if (zero) {
+    *out = 0.0;
+    return 0;
+  }
+  if (negative) return 5;
+  *out = exp(log_sum);
+  return 0;
+}
+
+__device__ __forceinline__ double clamp01(double r) {
+  return r < 0.0 ? 0.0 : (1.0 < r ? 1.0 : r);  // std::clamp(raw, 0, 1)
+}
+
+}  // namespace eigenid_b200

@@ -1,0 +1,327 @@
+// identity.cu — K3: the fused identity kernel (product stage of
+// all_magnitudes, identity.cpp:308-314 -> evaluate(), :185-238).
+//
+// For every (i, j) it forms exactly the reference's value: sorted pairing
+// (== reversed natural order), batches of B pairs, per batch
+// ratio = num/den, raw = product of ratios in batch order, log-domain retry
+// when raw is not finite, clamp to [0, 1].  Identical spectra therefore give
+// bit-identical output.
+//
+// B200 mapping:
+//  * The denominator product of a batch depends on (i, batch) only, so it is
+//    hoisted into a table den[i][b] (plus its correctly rounded reciprocal)
+//    built once by den_table_kernel: the inner loop is one DSUB + one DMUL
+//    per (i, j, k) triple instead of the reference's 2 DSUB + 2 DMUL.
+//  * The per-batch division num/den is a reciprocal multiply with one FMA
+//    correction (Markstein), which is correctly rounded whenever the quotient
+//    is in the normal range; outside it falls back to __ddiv_rn.
+//  * CTA tile: 256 i (lanes, 8 per thread, coalesced stores along i) x 32 j
+//    (8 warps x 4 rows); mu for the 32 rows is staged through shared memory
+//    in 64-wide k chunks with cp.async double buffering; inside a warp every
+//    mu load is a broadcast.
+#include "common.cuh"
+
+namespace eigenid_b200 {
+
+constexpr int kIdTI = 256;   // i per CTA
+constexpr int kIdTJ = 32;    // j per CTA
+constexpr int kIdQI = 8;     // i per thread
+constexpr int kIdPJ = 4;     // j per thread (per warp)
+constexpr int kIdCH = 64;    // k chunk staged in shared memory
+
+// den[i*nb + b] = prod over batch b (sorted order) of (lambda_i - lambda_k'),
+// rcp = RN(1/den).  Same multiplication order as identity.cpp:206-213.
+__global__ void den_table_kernel(const double* __restrict__ lam, int n,
+                                 int batch, int nb, double* __restrict__ den,
+                                 double* __restrict__ rcp) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n * nb) return;
+  const int i = (int)(t / nb), b = (int)(t % nb);
+  const double li = lam[i];
+  const int s0 = b * batch, s1 = min(s0 + batch, n - 1);
+  double dn = 1.0;
+  for (int s = s0; s < s1; ++s) {
+    const int k = n - 2 - s;
+    dn = __dmul_rn(dn, __dsub_rn(li, lam[k + (k >= i)]));
+  }
+  den[t] = dn;
+  rcp[t] = __drcp_rn(dn);
+}
+
+__device__ __forceinline__ double div_rn_fast(double a, double b, double r) {
+  const double q = __dmul_rn(a, r);
+  const double res = __fma_rn(-q, b, a);
+  const double q2 = __fma_rn(res, r, q);
+  const double aq = fabs(q2);
+  if (!(aq >= 1e-290 && aq <= 1e290) || !(fabs(a) >= 1e-290) ||
+      !(fabs(b) >= 1e-290 && fabs(b) <= 1e290))
+    return __ddiv_rn(a, b);
+  return q2;
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void cp_async_wait_1() {
+  asm volatile("cp.async.wait_group 1;\n" ::);
+}
+__device__ __forceinline__ void cp_async_wait_0() {
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// Stages mu rows [jt, jt+32) for sorted indices s in [s0, s0+64) as
+// smu[row][s - s0] = mu_row[n-2-s] (rows past `rows` clamp to the last row;
+// s past n-2 is padding and never consumed).
+__device__ __forceinline__ void stage_mu(double* smu, const double* mu,
+                                         long long ldmu, int rows, int jt,
+                                         int n, int s0) {
+  for (int t = threadIdx.x; t < kIdTJ * kIdCH; t += blockDim.x) {
+    const int r = t / kIdCH, c = t % kIdCH;
+    const int row = min(jt + r, rows - 1);
+    const int s = min(s0 + c, n - 2);
+    cp_async8(smu + r * (kIdCH + 1) + c, mu + row * ldmu + (n - 2 - s));
+  }
+}
+
+// out row r (= minor j0 + r), column i.  mu row r likewise.  flags collects
+// (r, i) pairs whose raw product is not finite, for the log-domain retry.
+__global__ void __launch_bounds__(256, 1)
+identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
+                int n, int rows, int batch, int nb,
+                const double* __restrict__ den, const double* __restrict__ rcp,
+                double* __restrict__ out, unsigned long long* flag_count,
+                long long* flags, long long flag_cap) {
+  __shared__ double smu[2][kIdTJ * (kIdCH + 1)];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = blockIdx.x * kIdTI, jt = blockIdx.y * kIdTJ;
+  const long long ldmu = n - 1;
+
+  double li[kIdQI];
+  int ii[kIdQI];
+#pragma unroll
+  for (int q = 0; q < kIdQI; ++q) {
+    ii[q] = i0 + lane + 32 * q;
+    li[q] = lam[min(ii[q], n - 1)];
+  }
+  double acc[kIdQI][kIdPJ], num[kIdQI][kIdPJ];
+#pragma unroll
+  for (int q = 0; q < kIdQI; ++q)
+#pragma unroll
+    for (int p = 0; p < kIdPJ; ++p) {
+      acc[q][p] = 1.0;
+      num[q][p] = 1.0;
+    }
+
+  const int total = n - 1;  // number of factor pairs
+  const int nchunks = (total + kIdCH - 1) / kIdCH;
+  stage_mu(smu[0], mu, ldmu, rows, jt, n, 0);
+  cp_async_commit();
+  int batch_end = min(batch, total);
+  int b = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      stage_mu(smu[(c + 1) & 1], mu, ldmu, rows, jt, n, (c + 1) * kIdCH);
+      cp_async_commit();
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_0();
+    }
+    __syncthreads();
+    const double* sm = smu[c & 1] + (warp * kIdPJ) * (kIdCH + 1);
+    const int s0 = c * kIdCH, s1 = min(s0 + kIdCH, total);
+    int s = s0;
+    while (s < s1) {
+      const int stop = min(s1, batch_end);
+      for (; s < stop; ++s) {
+        double m[kIdPJ];
+#pragma unroll
+        for (int p = 0; p < kIdPJ; ++p) m[p] = sm[p * (kIdCH + 1) + (s - s0)];
+#pragma unroll
+        for (int q = 0; q < kIdQI; ++q)
+#pragma unroll
+          for (int p = 0; p < kIdPJ; ++p)
+            num[q][p] = __dmul_rn(num[q][p], __dsub_rn(li[q], m[p]));
+      }
+      if (s == batch_end) {
+#pragma unroll
+        for (int q = 0; q < kIdQI; ++q) {
+          const long long t = (long long)min(ii[q], n - 1) * nb + b;
+          const double dq = den[t], rq = rcp[t];
+#pragma unroll
+          for (int p = 0; p < kIdPJ; ++p) {
+            acc[q][p] = __dmul_rn(acc[q][p], div_rn_fast(num[q][p], dq, rq));
+            num[q][p] = 1.0;
+          }
+        }
+        ++b;
+        batch_end = min(batch_end + batch, total);
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int p = 0; p < kIdPJ; ++p) {
+    const int r = jt + warp * kIdPJ + p;
+    if (r >= rows) continue;
+    double* orow = out + (long long)r * n;
+#pragma unroll
+    for (int q = 0; q < kIdQI; ++q) {
+      if (ii[q] >= n) continue;
+      const double raw = acc[q][p];
+      if (isfinite(raw)) {
+        orow[ii[q]] = clamp01(raw);
+      } else {
+        const unsigned long long slot = atomicAdd(flag_count, 1ull);
+        if ((long long)slot < flag_cap) flags[slot] = (long long)r * n + ii[q];
+      }
+    }
+  }
+}
+
+// Log-domain retry for flagged components (identity.cpp:227-231), and the
+// whole stage when IdentityConfig::Evaluation::kLogDomain is selected.
+__global__ void log_domain_fix_kernel(const double* __restrict__ lam,
+                                      const double* __restrict__ mu, int n,
+                                      const unsigned long long* flag_count,
+                                      const long long* flags,
+                                      double* __restrict__ out,
+                                      DevStatus* status) {
+  const unsigned long long cnt = *flag_count;
+  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x +
+                              threadIdx.x;
+       t < cnt; t += (unsigned long long)gridDim.x * blockDim.x) {
+    const long long idx = flags[t];
+    const int r = (int)(idx / n), i = (int)(idx % n);
+    double v;
+    const int rc = identity_log_domain(lam, mu + (long long)r * (n - 1), n, i, &v);
+    if (rc)
+      set_status(status, rc, i, 0.0, r);
+    else
+      out[idx] = clamp01(v);
+  }
+}
+
+__global__ void log_domain_all_kernel(const double* __restrict__ lam,
+                                      const double* __restrict__ mu, int n,
+                                      int rows, double* __restrict__ out,
+                                      DevStatus* status) {
+  const long long total = (long long)rows * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(t / n), i = (int)(t % n);
+    double v;
+    const int rc = identity_log_domain(lam, mu + (long long)r * (n - 1), n, i, &v);
+    if (rc)
+      set_status(status, rc, i, 0.0, r);
+    else
+      out[t] = clamp01(v);
+  }
+}
+
+// check_fully_nondegenerate (identity.cpp:141-149) on the device.
+__global__ void degeneracy_kernel(const double* __restrict__ lam, int n,
+                                  double tol, DevStatus* status) {
+  const double range = lam[n - 1] - lam[0];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k + 1 < n;
+       k += gridDim.x * blockDim.x) {
+    const double g = lam[k + 1] - lam[k];
+    if (g <= tol * range) {
+      // lowest k wins, as in the reference's sequential scan
+      atomicMin((unsigned long long*)&status[1].index, (unsigned long long)k);
+      status[1].code = 2;
+    }
+  }
+}
+
+__global__ void degeneracy_finish_kernel(const double* __restrict__ lam,
+                                         DevStatus* status) {
+  if (status[1].code == 2 && status[0].code == 0) {
+    const long long k = status[1].index;
+    status[0].code = 2;
+    status[0].index = k;
+    status[0].gap = lam[k + 1] - lam[k];
+  }
+}
+
+// C5 synthetic minor spectra, bit-identical to orc_c5_mu_row.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void c5_mu_kernel(uint64_t seed, const double* __restrict__ lam,
+                             int n, int j0, int rows, double* __restrict__ mu) {
+  const long long total = (long long)rows * (n - 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / (n - 1);
+    const int k = (int)(t % (n - 1));
+    const uint64_t j = (uint64_t)(j0 + r);
+    const uint64_t h = splitmix64(seed ^ ((j << 32) ^ (uint64_t)k));
+    const double u = __dmul_rn(__dadd_rn((double)(h >> 11), 0.5), 0x1.0p-53);
+    const double lo = lam[k], hi = lam[k + 1];
+    const double w = __dsub_rn(hi, lo);
+    double v = __dadd_rn(lo, __dmul_rn(u, w));
+    if (!(v > lo && v < hi)) v = __dmul_rn(0.5, __dadd_rn(lo, hi));
+    mu[t] = v;
+  }
+}
+
+// ---- launchers ----------------------------------------------------------
+
+int identity_nb(int n, int batch) { return (n - 1 + batch - 1) / batch; }
+
+cudaError_t launch_identity(const double* dlam, const double* dmu, int n,
+                            int rows, int batch, double* dden, double* drcp,
+                            double* dout, unsigned long long* dflag_count,
+                            long long* dflags, long long flag_cap,
+                            DevStatus* dstatus, int log_domain,
+                            cudaStream_t st, int* launches) {
+  if (rows <= 0) return cudaSuccess;
+  if (log_domain) {
+    log_domain_all_kernel<<<148 * 8, 256, 0, st>>>(dlam, dmu, n, rows, dout,
+                                                   dstatus);
+    ++*launches;
+    return cudaGetLastError();
+  }
+  const int nb = identity_nb(n, batch);
+  const long long nt = (long long)n * nb;
+  den_table_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(dlam, n, batch,
+                                                                 nb, dden, drcp);
+  cudaMemsetAsync(dflag_count, 0, sizeof(unsigned long long), st);
+  dim3 grid((n + kIdTI - 1) / kIdTI, (rows + kIdTJ - 1) / kIdTJ);
+  identity_kernel<<<grid, 256, 0, st>>>(dlam, dmu, n, rows, batch, nb, dden,
+                                        drcp, dout, dflag_count, dflags,
+                                        flag_cap);
+  log_domain_fix_kernel<<<148, 256, 0, st>>>(dlam, dmu, n, dflag_count, dflags,
+                                             dout, dstatus);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_degeneracy(const double* dlam, int n, double tol,
+                              DevStatus* dstatus, cudaStream_t st,
+                              int* launches) {
+  degeneracy_kernel<<<(n + 255) / 256, 256, 0, st>>>(dlam, n, tol, dstatus);
+  degeneracy_finish_kernel<<<1, 1, 0, st>>>(dlam, dstatus);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_c5_mu(uint64_t seed, const double* dlam, int n, int j0,
+                         int rows, double* dmu, cudaStream_t st,
+                         int* launches) {
+  c5_mu_kernel<<<148 * 16, 256, 0, st>>>(seed, dlam, n, j0, rows, dmu);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace eigenid_b200

@@ -1,0 +1,314 @@
+"""Python mirror of the reference's public API for the hot path.
+
+Same names, argument meaning and error behaviour as
+proj/include/eigenid/{matrix,eigensolve,identity}.hpp, implemented over the
+C-ABI (include/eigenid_b200.h) — every computation runs in the sm_100a
+kernels of libeigenid_b200.so; nothing here computes eigenvalues or
+products on the CPU.
+
+    SymmetricMatrix.build        matrix.hpp:21-22, matrix.cpp:10-38
+    SymmetricMatrix.minor_matrix matrix.hpp:35-37, matrix.cpp:51-68
+    eigenvalues(a)               eigensolve.hpp:46, eigensolve.cpp:130-132
+    IdentityConfig               identity.hpp:81-93
+    IdentityEngine.all_magnitudes identity.hpp:133-135, identity.cpp:294-316
+    eigenvalue_solve_count       identity.hpp:137-144
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, errors
+
+KSTRICT, KSYMMETRIZE = "strict", "symmetrize"
+
+
+class SymmetricMatrix:
+    """Dense real symmetric n x n matrix, row-major, immutable
+    (matrix.hpp:13-47)."""
+
+    def __init__(self, n: int, entries: np.ndarray):
+        self._n = n
+        self._e = entries
+        self._e.setflags(write=False)
+
+    @staticmethod
+    def build(n: int, entries, policy: str = KSTRICT) -> "SymmetricMatrix":
+        """matrix.cpp:10-38: DimensionMismatch / NonFiniteEntry /
+        AsymmetricInput (strict) or (A + A^T)/2 off the diagonal (symmetrize)."""
+        if n < 1:
+            raise errors.DimensionMismatch("matrix dimension must be >= 1")
+        e = np.array(entries, dtype=np.float64).reshape(-1)
+        if e.size != n * n:
+            raise errors.DimensionMismatch(
+                f"expected {n * n} entries, got {e.size}")
+        if not np.all(np.isfinite(e)):
+            raise errors.NonFiniteEntry("matrix entry is not finite")
+        m = e.reshape(n, n)
+        up = np.triu_indices(n, 1)
+        asym = np.abs(m[up] - m.T[up])
+        max_asym = float(asym.max()) if asym.size else 0.0
+        if max_asym > 0.0:
+            if policy == KSTRICT:
+                raise errors.AsymmetricInput(
+                    f"input is not symmetric (max |a_rc - a_cr| = {max_asym:f})")
+            mid = 0.5 * (m[up] + m.T[up])
+            m = m.copy()
+            m[up] = mid
+            m.T[up] = mid
+            e = m.reshape(-1)
+        return SymmetricMatrix(n, np.ascontiguousarray(e))
+
+    @staticmethod
+    def diagonal(d) -> "SymmetricMatrix":
+        d = np.asarray(d, dtype=np.float64)
+        return SymmetricMatrix.build(d.size, np.diag(d))
+
+    @staticmethod
+    def identity(n: int) -> "SymmetricMatrix":
+        return SymmetricMatrix.diagonal(np.ones(n))
+
+    def n(self) -> int:
+        return self._n
+
+    def entries(self) -> np.ndarray:
+        return self._e
+
+    def array(self) -> np.ndarray:
+        return self._e.reshape(self._n, self._n)
+
+    def __call__(self, r: int, c: int) -> float:
+        return float(self._e[r * self._n + c])
+
+    def minor_matrix(self, j: int) -> "SymmetricMatrix":
+        """matrix.cpp:51-68."""
+        if self._n == 1:
+            raise errors.MatrixTooSmall("cannot take a minor of a 1x1 matrix")
+        if j >= self._n or j < 0:
+            raise errors.IndexOutOfRange(
+                f"minor index {j} out of range for n = {self._n}")
+        keep = np.r_[0:j, j + 1:self._n]
+        m = self.array()[np.ix_(keep, keep)]
+        return SymmetricMatrix(self._n - 1, np.ascontiguousarray(m).reshape(-1))
+
+    def scaled(self, factor: float) -> "SymmetricMatrix":
+        return SymmetricMatrix(self._n, self._e * factor)
+
+    def frobenius_norm(self) -> float:
+        return float(np.sqrt(np.sum(self._e * self._e)))
+
+    def trace(self) -> float:
+        return float(np.trace(self.array()))
+
+
+def _as_matrix(a) -> tuple[int, np.ndarray]:
+    if isinstance(a, SymmetricMatrix):
+        return a.n(), np.ascontiguousarray(a.entries())
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if arr.ndim != 2 or arr.shape[0] != arr.shape[1]:
+        raise errors.DimensionMismatch("expected a square matrix")
+    return arr.shape[0], arr.reshape(-1)
+
+
+@dataclass
+class IdentityConfig:
+    """identity.hpp:81-93.  `workers` is accepted for source compatibility and
+    has no device meaning (the CUDA grid replaces the thread pool)."""
+    batch_size: int = 64
+    workers: int = 0
+    degeneracy_tol: float = 1e-12
+    evaluation: str = "paired-batched"  # or "log-domain"
+
+    def _c(self) -> _native.GpuConfig:
+        return _native.GpuConfig(int(self.batch_size), float(self.degeneracy_tol),
+                                 1 if self.evaluation == "log-domain" else 0)
+
+
+class Device:
+    """One C-ABI context (device buffers + stream), shared by engines on the
+    same GPU like the reference's per-engine pool (SPEC D5)."""
+
+    _instances: dict[int, "Device"] = {}
+    _lock = threading.Lock()
+
+    def __init__(self, device: int = 0):
+        self.lib = _native.load()
+        self.ctx = C.c_void_p()
+        err = _native.GpuErr()
+        _native.check(self.lib.eigenid_gpu_create(C.byref(self.ctx), device,
+                                                  C.byref(err)), err)
+        self.device = device
+
+    @classmethod
+    def get(cls, device: int = 0) -> "Device":
+        with cls._lock:
+            if device not in cls._instances:
+                cls._instances[device] = Device(device)
+            return cls._instances[device]
+
+    def stream(self) -> int:
+        return int(self.lib.eigenid_gpu_stream(self.ctx) or 0)
+
+    def launch_count(self) -> int:
+        return int(self.lib.eigenid_gpu_launch_count(self.ctx))
+
+    def sync(self):
+        err = _native.GpuErr()
+        _native.check(self.lib.eigenid_gpu_sync(self.ctx, C.byref(err)), err)
+
+    def __del__(self):
+        try:
+            if self.ctx:
+                self.lib.eigenid_gpu_destroy(self.ctx)
+        except Exception:
+            pass
+
+
+def eigenvalues(a, device: int = 0) -> np.ndarray:
+    """Spectrum eigenvalues(const SymmetricMatrix&): ascending eigenvalues,
+    computed on the GPU (stage 1 + stage 2 + Sturm bisection)."""
+    n, e = _as_matrix(a)
+    dev = Device.get(device)
+    out = np.empty(n, np.float64)
+    err = _native.GpuErr()
+    _native.check(dev.lib.eigenid_gpu_eigenvalues(dev.ctx, _native.dptr(e), n,
+                                                  _native.dptr(out), C.byref(err)),
+                  err)
+    return out
+
+
+class IdentityEngine:
+    """identity.hpp:99-157, the all-magnitudes path on the GPU."""
+
+    def __init__(self, cfg: IdentityConfig | None = None, device: int = 0):
+        self._cfg = cfg or IdentityConfig()
+        if self._cfg.batch_size < 1:
+            raise errors.ConfigError("batch size must be >= 1")
+        if not self._cfg.degeneracy_tol >= 0.0:
+            raise errors.ConfigError("degeneracy tolerance must be >= 0")
+        self._dev = Device.get(device)
+        self._solves = 0
+        self._solves_lock = threading.Lock()
+
+    def config(self) -> IdentityConfig:
+        return self._cfg
+
+    @property
+    def device(self) -> Device:
+        return self._dev
+
+    # -- instrumentation (identity.hpp:137-144)
+    def eigenvalue_solve_count(self) -> int:
+        return self._solves
+
+    def reset_solve_count(self) -> None:
+        self._solves = 0
+
+    def _count(self, before: int):
+        after = int(self._dev.lib.eigenid_gpu_solve_count(self._dev.ctx))
+        with self._solves_lock:
+            self._solves += after - before
+
+    def _before(self) -> int:
+        return int(self._dev.lib.eigenid_gpu_solve_count(self._dev.ctx))
+
+    def all_magnitudes(self, a, return_spectra: bool = False):
+        """Row-major n*n vector, entry [j*n + i] = |v_ij|^2
+        (identity.cpp:294-316)."""
+        n, e = _as_matrix(a)
+        lib = self._dev.lib
+        out = np.empty(n * n, np.float64)
+        lam = np.empty(max(n, 1), np.float64)
+        mu = np.empty(max(n * (n - 1), 1), np.float64) if return_spectra else None
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        b = self._before()
+        st = lib.eigenid_gpu_all_magnitudes(
+            self._dev.ctx, _native.dptr(e), n, C.byref(cfg), _native.dptr(out),
+            _native.dptr(lam), _native.dptr(mu) if mu is not None else None,
+            C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        if return_spectra:
+            return out, lam[:n], mu[: n * (n - 1)].reshape(n, n - 1)
+        return out
+
+    def all_magnitudes_batched(self, a_batch) -> np.ndarray:
+        """count x n x n independent matrices -> count x n*n (config C2)."""
+        a_batch = np.ascontiguousarray(np.asarray(a_batch, dtype=np.float64))
+        count, n = a_batch.shape[0], a_batch.shape[1]
+        out = np.empty((count, n * n), np.float64)
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        b = self._before()
+        st = self._dev.lib.eigenid_gpu_all_magnitudes_batched(
+            self._dev.ctx, _native.dptr(a_batch), count, n, C.byref(cfg),
+            _native.dptr(out), C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        return out
+
+    def minor_spectra(self, a, j0: int = 0, j1: int | None = None):
+        """lambda(A) and the ascending spectra of minors j0..j1-1."""
+        n, e = _as_matrix(a)
+        j1 = n if j1 is None else j1
+        lam = np.empty(n, np.float64)
+        mu = np.empty((max(j1 - j0, 1), n - 1), np.float64)
+        err = _native.GpuErr()
+        b = self._before()
+        st = self._dev.lib.eigenid_gpu_minor_spectra(
+            self._dev.ctx, _native.dptr(e), n, j0, j1, _native.dptr(lam),
+            _native.dptr(mu), C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        return lam, mu[: j1 - j0]
+
+    def identity(self, lam, mu_rows, j0: int = 0) -> np.ndarray:
+        """Identity stage only from given spectra (rows j0..j0+len(mu_rows))."""
+        lam = np.ascontiguousarray(lam, np.float64)
+        mu_rows = np.ascontiguousarray(mu_rows, np.float64)
+        n = lam.shape[0]
+        rows = mu_rows.shape[0]
+        out = np.empty((rows, n), np.float64)
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        _native.check(self._dev.lib.eigenid_gpu_identity(
+            self._dev.ctx, _native.dptr(lam), _native.dptr(mu_rows), n, j0,
+            j0 + rows, C.byref(cfg), _native.dptr(out), C.byref(err)), err)
+        return out
+
+    # -- device-resident entry points (torch tensors or raw pointers)
+    def all_magnitudes_device(self, a_ptr: int, n: int, j0: int, j1: int,
+                              out_ptr: int, lam_ptr: int = 0, mu_ptr: int = 0):
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        _native.check(self._dev.lib.eigenid_gpu_all_magnitudes_device(
+            self._dev.ctx, a_ptr, n, j0, j1, C.byref(cfg), out_ptr,
+            lam_ptr or None, mu_ptr or None, C.byref(err)), err)
+
+    def identity_device(self, lam_ptr: int, mu_ptr: int, n: int, j0: int,
+                        j1: int, out_ptr: int):
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        _native.check(self._dev.lib.eigenid_gpu_identity_device(
+            self._dev.ctx, lam_ptr, mu_ptr, n, j0, j1, C.byref(cfg), out_ptr,
+            C.byref(err)), err)
+
+    def batched_device(self, a_ptr: int, count: int, n: int, out_ptr: int):
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        _native.check(self._dev.lib.eigenid_gpu_all_magnitudes_batched_device(
+            self._dev.ctx, a_ptr, count, n, C.byref(cfg), out_ptr, C.byref(err)),
+            err)
+
+    def c5_mu_device(self, seed: int, lam_ptr: int, n: int, j0: int, j1: int,
+                     mu_ptr: int):
+        err = _native.GpuErr()
+        _native.check(self._dev.lib.eigenid_gpu_c5_mu_device(
+            self._dev.ctx, seed, lam_ptr, n, j0, j1, mu_ptr, C.byref(err)), err)
+
+    def sync(self):
+        self._dev.sync()
