@@ -16,6 +16,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -248,6 +249,38 @@ int begin(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
   return EIGENID_OK;
 }
 
+// EIGENID_PROFILE=1 prints per-stage device times of run_large to stderr
+// (development aid; the bench times whole steps with its own events).
+struct StageTimer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> names;
+  explicit StageTimer(cudaStream_t s) : st(s) {
+    const char* e = std::getenv("EIGENID_PROFILE");
+    on = e && e[0] == '1';
+    mark("start");
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    names.push_back(name);
+  }
+  ~StageTimer() {
+    if (!on) return;
+    cudaEventSynchronize(ev.back());
+    for (size_t t = 1; t < ev.size(); ++t) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[t - 1], ev[t]);
+      std::fprintf(stderr, "[eigenid] %-14s %10.3f ms\n", names[t], ms);
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
 // Large-n pipeline for minor rows [j0, j1) of a device matrix.
 int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
               const eigenid_gpu_config* cfg, double* dout, double* dlam,
@@ -273,18 +306,22 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   solve_list_kernel<<<(nsolves + 255) / 256, 256, 0, st>>>(djs, j0, rows);
   ++launches;
 
+  StageTimer timer(st);
   Stage1Args s1{dA, n, djs, nsolves, c->bWs.as<double>(), ws_stride, ldw,
                 c->bBand.as<double>(), band_stride};
   EID_CUDA(launch_stage1(s1, slots, st), "stage1");
+  timer.mark("stage1");
   ++launches;
   Stage2Args s2{c->bBand.as<double>(), band_stride, djs, nsolves, n,
                 c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(), n};
   EID_CUDA(launch_stage2(s2, st), "stage2");
   ++launches;
+  timer.mark("stage2");
   // lambda(A): Gershgorin brackets, split across CTAs
   BisectArgs ba{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
                 n, djs, nsolves, 0, n, nullptr, dlam, n, (n + 255) / 256};
   EID_CUDA(launch_bisect(ba, 1, n, st, &launches), "bisect A");
+  timer.mark("bisect_A");
   if (identity) EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol,
                                            c->dstatus, st, &launches),
                          "degeneracy");
@@ -292,6 +329,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
     BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
                   n, djs, nsolves, 1, n, dlam, dmu, n - 1, 1};
     EID_CUDA(launch_bisect(bm, rows, n - 1, st, &launches), "bisect minors");
+    timer.mark("bisect_minors");
   }
   if (identity && rows > 0) {
     const int batch = batch_of(cfg, n);
@@ -307,6 +345,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
                              c->bFlags.as<long long>(), cap, c->dstatus,
                              cfg->log_domain, st, &launches),
              "identity");
+    timer.mark("identity");
   }
   c->launches += launches;
   return EIGENID_OK;

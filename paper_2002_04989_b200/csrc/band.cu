@@ -25,17 +25,24 @@ constexpr int kB = 32;      // bandwidth / panel width
 constexpr int kNT = 256;    // threads per CTA (8 warps)
 constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
-// Shared-memory layout (doubles).
-constexpr int kG1_LDA = 36, kG1_LDB = 36;            // GEMM1 tiles
-constexpr int kG1_A = 64 * kG1_LDA, kG1_B = 32 * kG1_LDB;
-constexpr int kG2_LD = 68;                            // GEMM2 operand tiles
-constexpr int kG2_OP = 64 * kG2_LD;
-constexpr int kGemmSmem = (2 * kG1_A + 2 * kG1_B) > (3 * kG2_OP)
-                              ? (2 * kG1_A + 2 * kG1_B)
-                              : (3 * kG2_OP);
+// Shared-memory layout (doubles).  One CTA (8 warps) per SM; the GEMM
+// region is reused by the panel / Gram phases.
+constexpr int kG2M = 128, kG2N = 64, kG2K = 2 * kB, kG2LD = kG2K + 4;  // 68
+constexpr int kG2_A = kG2M * kG2LD;                 // Aop  128 x 64
+constexpr int kG2_B = kG2N * kG2LD;                 // Bop   64 x 64 (x2)
+constexpr int kG1M = 128, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 132;
+constexpr int kG1_A = kG1M * kG1LDA;                // pass 1: A chunk 128 x 32
+constexpr int kG1_T = kG1K * kG1TLD;                // pass 2: A chunk 32 x 128
+constexpr int kG1_B = kG1K * kG1LDB;                // VT chunk 32 x 32
 constexpr int kSmallLD = kB + 1;
-constexpr int kSmallMat = kB * kSmallLD;  // T, G/Y, M
-constexpr int kStage1SmemDoubles = kGemmSmem + 3 * kSmallMat + 8 * kB + 4 * kB;
+constexpr int kSmallMat = kB * kSmallLD;            // T, G/Y, M
+constexpr int kGramPart = 8 * kSmallMat;
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int kGemmSmem =
+    cmax(cmax(kG2_A + 2 * kG2_B, 2 * (kG1_A + kG1_B)),
+         cmax(2 * (kG1_T + kG1_B), kGramPart));
+constexpr int kRed = 8 + 8 * kB;
+constexpr int kStage1SmemDoubles = kGemmSmem + 6 * kSmallMat + kRed + 4 * kB;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile(
@@ -54,22 +61,6 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem,
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-// Reduce-scatter of 32 per-lane values: afterwards lane l holds the warp sum
-// of vals[l] in vals[0].
-__device__ __forceinline__ void warp_reduce_scatter32(double (&v)[kB]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int q = 0; q < o; ++q) {
-      const double send = up ? v[q] : v[q + o];
-      const double keep = up ? v[q + o] : v[q];
-      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-}
 
 __device__ __forceinline__ double block_sum(double x, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -96,26 +87,24 @@ struct Stage1Args {
 };
 
 // ---- panel QR ----------------------------------------------------------
-// Householder QR of the s x kB panel P(r,t) = W[(c0+r)*ldw + cp + t]
-// (LAPACK dgeqr2 / dlarfg convention: H = I - tau v v^T, v_0 = 1).
-// R overwrites the panel's upper triangle, zeros below; V (s x kB,
-// row-major, unit lower trapezoidal, zero above) goes to Vg; tau to stau.
-__device__ void panel_qr(double* W, int ldw, int c0, int cp, int s, double* Vg,
-                         double* stau, double* red, double* wsm) {
+// Householder QR of the s x kB panel P(r,q) = P0[r*ldw + q] (LAPACK
+// dgeqr2/dlarfg convention, H = I - tau v v^T, v_0 = 1).  Lane q owns column
+// q, warps stride over rows, so every row access is one coalesced 256-byte
+// warp load; two streaming passes per column (w = v^T P, then the update
+// fused with the next column's norm).  On exit the upper triangle holds R and
+// the strictly lower part holds the reflectors v (LAPACK layout).
+__device__ void panel_qr(double* P0, int ldw, int s, double* stau, double* red,
+                         double* wsm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kr = min(kB, s - 1);
-  auto P = [&](int r, int t) -> double& {
-    return W[(long long)(c0 + r) * ldw + cp + t];
-  };
-  // sigma for column 0
   double loc = 0.0;
   for (int r = 1 + tid; r < s; r += kNT) {
-    const double x = P(r, 0);
+    const double x = P0[(long long)r * ldw];
     loc += x * x;
   }
   double sigma = block_sum(loc, red);
   for (int t = 0; t < kr; ++t) {
-    const double alpha = P(t, t);
+    const double alpha = P0[(long long)t * ldw + t];
     double tau, beta, scal;
     if (sigma == 0.0) {
       tau = 0.0;
@@ -126,238 +115,566 @@ __device__ void panel_qr(double* W, int ldw, int c0, int cp, int s, double* Vg,
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    // v below the diagonal; w_q = P(t,q) + sum_{r>t} v_r P(r,q), q > t
-    double acc[kB];
+    // pass A: acc_q = sum_{r>t} P(r,t) P(r,q)
+    double acc = 0.0;
+    for (int r0 = t + 1 + warp; r0 < s; r0 += 32) {
+      double row[4];
 #pragma unroll
-    for (int q = 0; q < kB; ++q) acc[q] = 0.0;
-    for (int r = t + 1 + tid; r < s; r += kNT) {
-      double* prow = &P(r, 0);
-      const double v = prow[t] * scal;
-      Vg[(long long)r * kB + t] = v;
-      prow[t] = 0.0;
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 8 * u;
+        row[u] = r < s ? P0[(long long)r * ldw + lane] : 0.0;
+      }
 #pragma unroll
-      for (int q = 0; q < kB; ++q)
-        if (q > t) acc[q] += v * prow[q];
+      for (int u = 0; u < 4; ++u)
+        acc += __shfl_sync(0xffffffffu, row[u], t) * row[u];
     }
-    warp_reduce_scatter32(acc);
     __syncthreads();
-    red[8 + warp * kB + lane] = acc[0];
+    red[8 + warp * kB + lane] = acc;
     __syncthreads();
-    if (tid < kB) {
+    if (warp == 0) {
       double w = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < kNT / 32; ++ww) w += red[8 + ww * kB + tid];
-      wsm[tid] = (tid > t) ? tau * (w + P(t, tid)) : 0.0;
+      for (int ww = 0; ww < kNT / 32; ++ww) w += red[8 + ww * kB + lane];
+      w = w * scal + P0[(long long)t * ldw + lane];
+      wsm[lane] = (lane > t) ? tau * w : 0.0;
     }
     __syncthreads();
-    // apply: P(r,q) -= tau w_q v_r (r >= t, q > t); accumulate next sigma
+    // pass B: P(r,q) -= tau w_q v_r, v stored below the diagonal
+    const double wq = wsm[lane];
     loc = 0.0;
-    for (int r = t + tid; r < s; r += kNT) {
-      double* prow = &P(r, 0);
-      const double v = (r == t) ? 1.0 : Vg[(long long)r * kB + t];
+    for (int r0 = t + warp; r0 < s; r0 += 32) {
+      double row[4];
 #pragma unroll
-      for (int q = 0; q < kB; ++q)
-        if (q > t) prow[q] -= wsm[q] * v;
-      if (t + 1 < kB && r > t + 1) loc += prow[t + 1] * prow[t + 1];
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 8 * u;
+        row[u] = r < s ? P0[(long long)r * ldw + lane] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 8 * u;
+        if (r < s) {
+          const double x = __shfl_sync(0xffffffffu, row[u], t);
+          const double v = (r == t) ? 1.0 : x * scal;
+          double y = row[u];
+          if (lane > t)
+            y -= wq * v;
+          else if (lane == t)
+            y = (r == t) ? beta : v;
+          if (lane >= t) P0[(long long)r * ldw + lane] = y;
+          if (lane == t + 1 && r > t + 1) loc += y * y;
+        }
+      }
     }
-    if (tid == 0) {
-      P(t, t) = beta;
-      stau[t] = tau;
-      Vg[(long long)t * kB + t] = 1.0;
-    }
-    for (int r = tid; r < t; r += kNT) Vg[(long long)r * kB + t] = 0.0;
+    if (tid == 0) stau[t] = tau;
     sigma = block_sum(loc, red);
   }
-  // columns with no reflector (s - 1 < kB)
-  for (int t = kr; t < kB; ++t) {
-    for (int r = tid; r < s; r += kNT) Vg[(long long)r * kB + t] = 0.0;
-    if (tid == 0) stau[t] = 0.0;
+  if (tid < kB && tid >= kr) stau[tid] = 0.0;
+  __syncthreads();
+}
+
+// V (s x kB row-major, unit lower trapezoidal) from the LAPACK-layout panel.
+__device__ void extract_v(const double* P0, int ldw, int s, double* Vg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < s; r += kNT / 32) {
+    const double x = P0[(long long)r * ldw + lane];
+    Vg[(long long)r * kB + lane] = r > lane ? x : (r == lane ? 1.0 : 0.0);
   }
   __syncthreads();
 }
 
-// out[q][p] = sum_r L(r,q) R(r,p) over r in [0,s); L, R row-major s x kB.
-// Staged through shared memory in 64-row chunks (stg needs 2*64*(kB+1)).
-__device__ void gram(const double* Lg, const double* Rg, int s, double* out,
-                     double* stg) {
-  const int tid = threadIdx.x;
-  double* sL = stg;
-  double* sR = stg + 64 * kSmallLD;
-  const int p = tid & 31, q0 = tid >> 5;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int r0 = 0; r0 < s; r0 += 64) {
-    __syncthreads();
-    for (int t = tid; t < 64 * kB; t += kNT) {
-      const int r = t / kB, c = t % kB;
-      const bool ok = r0 + r < s;
-      sL[r * kSmallLD + c] = ok ? Lg[(long long)(r0 + r) * kB + c] : 0.0;
-      sR[r * kSmallLD + c] = ok ? Rg[(long long)(r0 + r) * kB + c] : 0.0;
-    }
-    __syncthreads();
-    const int rr = min(64, s - r0);
-    for (int r = 0; r < rr; ++r) {
-      const double rv = sR[r * kSmallLD + p];
+// out[q][p] = sum_{r<s} L(r,q) R(r,p) on the DMMA path: warp w takes the
+// 4-row k-slices i = w (mod 8); partials are summed through shared memory.
+__device__ void gram(const double* L, int ldl, const double* R, int ldr, int s,
+                     double* out, double* part) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = lane & 3, mm = lane >> 2;
+  double acc[4][4][2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += sL[r * kSmallLD + q0 + 8 * u] * rv;
-    }
-  }
-  __syncthreads();
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-  for (int u = 0; u < 4; ++u) out[(q0 + 8 * u) * kSmallLD + p] = acc[u];
-  __syncthreads();
-}
-
-// Y(r,:) = alpha * L(r,:) * Mt + (addg ? Add(r,:) : 0) for r in [0,s).
-// Mt is kB x kB in shared memory (ld kSmallLD).
-__device__ void row_transform(const double* Lg, const double* Mt, double alpha,
-                              const double* Add, double* Yg, int s) {
-  for (int r = threadIdx.x; r < s; r += kNT) {
-    double y[kB];
-#pragma unroll
-    for (int q = 0; q < kB; ++q) y[q] = 0.0;
-    const double* lr = Lg + (long long)r * kB;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll 2
+  for (int i = warp; 4 * i < s; i += kNT / 32) {
+    const int r = 4 * i + kk;
+    double a[4], b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      a[t] = r < s ? L[(long long)r * ldl + 8 * t + mm] : 0.0;
+      b[t] = r < s ? R[(long long)r * ldr + 8 * t + mm] : 0.0;
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+  }
+  __syncthreads();
+  double* pw = part + warp * kSmallMat;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      pw[(8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk] = acc[mt][nt][0];
+      pw[(8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk + 1] = acc[mt][nt][1];
+    }
+  __syncthreads();
+  for (int e = tid; e < kB * kB; e += kNT) {
+    const int q = e / kB, p = e % kB;
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kNT / 32; ++w) v += part[w * kSmallMat + q * kSmallLD + p];
+    out[q * kSmallLD + p] = v;
+  }
+  __syncthreads();
+}
+
+// Y(r,:) = (Add ? Add(r,:) : 0) + alpha * L(r,:) Mt, warp per row, lane per
+// output column (Mt in shared memory, ld kSmallLD).  In place is allowed.
+__device__ void row_transform(const double* L, int ldl, const double* Mt,
+                              double alpha, const double* Add, double* Y,
+                              int s) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r0 = warp; r0 < s; r0 += 2 * (kNT / 32)) {
+    double l[2], y[2] = {0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = r0 + 8 * u;
+      l[u] = r < s ? L[(long long)r * ldl + lane] : 0.0;
+    }
+#pragma unroll
     for (int p = 0; p < kB; ++p) {
-      const double lp = lr[p];
+      const double mv = Mt[p * kSmallLD + lane];
 #pragma unroll
-      for (int q = 0; q < kB; ++q) y[q] += lp * Mt[p * kSmallLD + q];
+      for (int u = 0; u < 2; ++u) y[u] += __shfl_sync(0xffffffffu, l[u], p) * mv;
     }
-    double* yr = Yg + (long long)r * kB;
-    const double* ar = Add ? Add + (long long)r * kB : nullptr;
 #pragma unroll
-    for (int q = 0; q < kB; ++q) yr[q] = (ar ? ar[q] : 0.0) + alpha * y[q];
+    for (int u = 0; u < 2; ++u) {
+      const int r = r0 + 8 * u;
+      if (r < s)
+        Y[(long long)r * kB + lane] =
+            (Add ? Add[(long long)r * kB + lane] : 0.0) + alpha * y[u];
+    }
   }
   __syncthreads();
 }
 
-// ---- GEMM 1: X(s x kB) = A22(s x s) * VT(s x kB) --------------------------
-__device__ void gemm1(const double* A22, int ldw, int s, const double* VTg,
-                      double* Xg, double* sm) {
+// ---- CholeskyQR2 panel with Householder reconstruction -----------------
+// The panel's Householder representation (V, T) is rebuilt from an
+// orthonormal basis Q1 of the panel (Ballard et al., "Reconstructing
+// Householder vectors from tall-skinny QR"): Q1 - S = L U with S = -sign of
+// each pivot, V = L, T = -U S L1^-T, and H = I - V T V^T satisfies
+// H^T P = [S R; 0].  Q1, R come from two Cholesky-QR passes (Gram matrices on
+// the DMMA path).  Five streaming passes over the panel replace the 2 kB
+// latency-bound passes of column Householder; panels whose second Gram
+// matrix is not within 1e-3 of I (cond(P) >~ 1e6), or whose Cholesky breaks
+// down, fall back to panel_qr.
+
+// Upper Cholesky factor R (G = R^T R) of the kB x kB matrix G; warp-level.
+__device__ bool warp_chol(const double* G, double* R) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  for (int j = 0; j < kB; ++j) {
+    double d = G[j * kSmallLD + j];
+    for (int k = 0; k < j; ++k) d -= R[k * kSmallLD + j] * R[k * kSmallLD + j];
+    if (!(d > 0.0)) ok = false;
+    const double rjj = sqrt(fmax(d, 1e-300));
+    if (lane > j) {
+      double v = G[j * kSmallLD + lane];
+      for (int k = 0; k < j; ++k) v -= R[k * kSmallLD + j] * R[k * kSmallLD + lane];
+      R[j * kSmallLD + lane] = v / rjj;
+    } else if (lane == j) {
+      R[j * kSmallLD + j] = rjj;
+    } else {
+      R[j * kSmallLD + lane] = 0.0;
+    }
+    __syncwarp();
+  }
+  return ok;
+}
+
+// Inverse of an upper triangular kB x kB matrix; lane c solves column c.
+__device__ void warp_upper_inv(const double* R, double* Ri) {
+  const int c = threadIdx.x & 31;
+  double x[kB];
+#pragma unroll
+  for (int i = kB - 1; i >= 0; --i) {
+    double v = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = i + 1; k < kB; ++k) v -= R[i * kSmallLD + k] * x[k];
+    x[i] = (i <= c) ? v / R[i * kSmallLD + i] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < kB; ++i) Ri[i * kSmallLD + c] = x[i];
+  __syncwarp();
+}
+
+// Inverse of a unit lower triangular matrix (strict lower part of L).
+__device__ void warp_unit_lower_inv(const double* L, double* Li) {
+  const int c = threadIdx.x & 31;
+  double x[kB];
+#pragma unroll
+  for (int i = 0; i < kB; ++i) {
+    double v = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) v -= L[i * kSmallLD + k] * x[k];
+    x[i] = (i >= c) ? v : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < kB; ++i) Li[i * kSmallLD + c] = x[i];
+  __syncwarp();
+}
+
+// C = A B for upper triangular A, B (kB x kB); lane c computes column c.
+__device__ void warp_upper_mul(const double* A, const double* B, double* C) {
+  const int c = threadIdx.x & 31;
+  for (int i = 0; i < kB; ++i) {
+    double v = 0.0;
+    for (int k = i; k <= c; ++k) v += A[i * kSmallLD + k] * B[k * kSmallLD + c];
+    C[i * kSmallLD + c] = (i <= c) ? v : 0.0;
+  }
+  __syncwarp();
+}
+
+__device__ bool chol_panel(double* P0, int ldw, int s, double* Vg, double* Xg,
+                           double* sT, double* sG, double* sA, double* sB,
+                           double* sR, double* sS, double* part, int* flag) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  gram(P0, ldw, P0, ldw, s, sG, part);                    // G1 = P^T P
+  if (warp == 0) {
+    const bool ok = warp_chol(sG, sA);                     // R1
+    if (lane == 0) *flag = ok;
+    if (ok) warp_upper_inv(sA, sB);                        // R1^-1
+  }
+  __syncthreads();
+  if (!*flag) return false;
+  row_transform(P0, ldw, sB, 1.0, nullptr, Vg, s);         // Q = P R1^-1
+  gram(Vg, kB, Vg, kB, s, sG, part);                      // G2 = Q^T Q
+  if (warp == 0) {
+    double dev = 0.0;
+    for (int e = lane; e < kB * kB; e += 32) {
+      const int q = e / kB, p = e % kB;
+      dev = fmax(dev, fabs(sG[q * kSmallLD + p] - (q == p ? 1.0 : 0.0)));
+    }
+    dev = warp_max(dev);
+    bool ok = dev <= 1e-3;
+    if (ok) ok = warp_chol(sG, sB);                        // R2
+    if (lane == 0) *flag = ok;
+    if (ok) {
+      warp_upper_mul(sB, sA, sR);                          // R = R2 R1
+      warp_upper_inv(sB, sA);                              // R2^-1
+    }
+  }
+  __syncthreads();
+  if (!*flag) return false;
+  row_transform(Vg, kB, sA, 1.0, nullptr, Xg, s);          // Q1 = Q R2^-1
+  if (warp == 0) {
+    // modified LU of the top block: Q1_top - S = L U (U' in sG upper)
+    for (int r = 0; r < kB; ++r) sG[r * kSmallLD + lane] = Xg[r * kB + lane];
+    __syncwarp();
+    for (int i = 0; i < kB; ++i) {
+      const double p = sG[i * kSmallLD + i];
+      const double si = p >= 0.0 ? -1.0 : 1.0;
+      __syncwarp();
+      if (lane == 0) {
+        sS[i] = si;
+        sG[i * kSmallLD + i] = p - si;
+      }
+      __syncwarp();
+      const double piv = sG[i * kSmallLD + i];
+      if (lane > i) {
+        const double l = sG[lane * kSmallLD + i] / piv;
+        sG[lane * kSmallLD + i] = l;
+        for (int c = i + 1; c < kB; ++c) sG[lane * kSmallLD + c] -= l * sG[i * kSmallLD + c];
+      }
+      __syncwarp();
+    }
+    // U'^-1 (upper part of sG) -> sB ; L1^-1 -> sA
+    {
+      const int c = lane;
+      double x[kB];
+#pragma unroll
+      for (int i = kB - 1; i >= 0; --i) {
+        double v = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = i + 1; k < kB; ++k) v -= sG[i * kSmallLD + k] * x[k];
+        x[i] = (i <= c) ? v / sG[i * kSmallLD + i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) sB[i * kSmallLD + c] = x[i];
+    }
+    __syncwarp();
+    warp_unit_lower_inv(sG, sA);
+  }
+  __syncthreads();
+  // T = -U' S L1^-T  (upper)
+  for (int e = tid; e < kB * kB; e += kNT) {
+    const int i = e / kB, jj = e % kB;
+    double v = 0.0;
+    for (int k = i; k <= jj; ++k)
+      v += sG[i * kSmallLD + k] * sS[k] * sA[jj * kSmallLD + k];
+    sT[i * kSmallLD + jj] = (i <= jj) ? -v : 0.0;
+  }
+  // V: top rows L1 (unit lower), below Q1_bottom U'^-1 ; panel top <- S R
+  for (int r = warp; r < kB; r += kNT / 32)
+    Vg[r * kB + lane] = lane < r ? sG[r * kSmallLD + lane] : (lane == r ? 1.0 : 0.0);
+  for (int r = warp; r < kB; r += kNT / 32)
+    P0[(long long)r * ldw + lane] = lane >= r ? sS[r] * sR[r * kSmallLD + lane] : 0.0;
+  __syncthreads();
+  row_transform(Xg + kB * kB, kB, sB, 1.0, nullptr, Vg + kB * kB, s - kB);
+  return true;
+}
+
+// ---- GEMM 1: X = A22 VT with A22 symmetric, lower triangle only ----------
+// pass 1: X[r] = sum_{c <= r} A(r,c) VT(c)       (row blocks of 128)
+// pass 2: X[c] += sum_{r > c} A(r,c) VT(r)       (column blocks of 128)
+// Elements outside the lower triangle are masked to zero in the fragments,
+// so only the lower triangle of A22 is ever read or kept up to date.
+__device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
+                      double* X, double* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = lane & 3, mm = lane >> 2;
   const int wm = warp >> 1, wn = warp & 1;
-  double* sA[2] = {sm, sm + kG1_A};
-  double* sB[2] = {sm + 2 * kG1_A, sm + 2 * kG1_A + kG1_B};
-  const int nk = (s + 31) / 32;
-  for (int rb = 0; rb < s; rb += 64) {
-    double acc[2][2][2];
+  // ---------------- pass 1
+  {
+    double* sA[2] = {sm, sm + kG1_A};
+    double* sB[2] = {sm + 2 * kG1_A, sm + 2 * kG1_A + kG1_B};
+    for (int rb = 0; rb < s; rb += kG1M) {
+      const int kend = min(rb + kG1M, s);
+      const int nk = (kend + kG1K - 1) / kG1K;
+      double acc[4][2][2];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    auto stage = [&](int kb, int buf) {
-      // A tile 64 x 32: 1024 16-byte chunks
-      for (int t = tid; t < 64 * 16; t += kNT) {
-        const int r = t >> 4, c2 = (t & 15) * 2;
-        const int gr = rb + r, gc = kb + c2;
-        int bytes = 0;
-        if (gr < s && gc < s) bytes = (gc + 1 < s) ? 16 : 8;
-        const double* src = bytes ? A22 + (long long)gr * ldw + gc : A22;
-        cp_async16(sA[buf] + r * kG1_LDA + c2, src, bytes);
-      }
-      // VT tile 32 x 32: 512 chunks
-      for (int t = tid; t < 32 * 16; t += kNT) {
-        const int r = t >> 4, c2 = (t & 15) * 2;
-        const int gr = kb + r;
-        const int bytes = gr < s ? 16 : 0;
-        const double* src = bytes ? VTg + (long long)gr * kB + c2 : VTg;
-        cp_async16(sB[buf] + r * kG1_LDB + c2, src, bytes);
-      }
-      cpa_commit();
-    };
-    __syncthreads();
-    stage(0, 0);
-    for (int ki = 0; ki < nk; ++ki) {
-      if (ki + 1 < nk) {
-        stage((ki + 1) * 32, (ki + 1) & 1);
-        cpa_wait1();
-      } else {
-        cpa_wait0();
-      }
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      auto stage = [&](int kb, int buf) {
+        for (int t = tid; t < kG1M * (kG1K / 2); t += kNT) {
+          const int r = t >> 4, c2 = (t & 15) * 2;
+          const int gr = rb + r, gc = kb + c2;
+          int bytes = 0;
+          if (gr < s && gc < kend) bytes = (gc + 1 < kend) ? 16 : 8;
+          cp_async16(sA[buf] + r * kG1LDA + c2,
+                     bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
+        }
+        for (int t = tid; t < kG1K * (kB / 2); t += kNT) {
+          const int r = t >> 4, c2 = (t & 15) * 2;
+          const int gr = kb + r;
+          const int bytes = gr < kend ? 16 : 0;
+          cp_async16(sB[buf] + r * kG1LDB + c2,
+                     bytes ? VT + (long long)gr * kB + c2 : VT, bytes);
+        }
+        cpa_commit();
+      };
       __syncthreads();
-      const double* a = sA[ki & 1];
-      const double* b = sB[ki & 1];
+      stage(0, 0);
+      for (int ki = 0; ki < nk; ++ki) {
+        if (ki + 1 < nk) {
+          stage((ki + 1) * kG1K, (ki + 1) & 1);
+          cpa_wait1();
+        } else {
+          cpa_wait0();
+        }
+        __syncthreads();
+        const double* a = sA[ki & 1];
+        const double* b = sB[ki & 1];
+        const int kb = ki * kG1K;
+        const bool diag = kb + kG1K > rb;  // chunk may cross the diagonal
 #pragma unroll
-      for (int k4 = 0; k4 < 8; ++k4) {
-        const int kk = 4 * k4 + (lane & 3);
-        const double a0 = a[(16 * wm + (lane >> 2)) * kG1_LDA + kk];
-        const double a1 = a[(16 * wm + 8 + (lane >> 2)) * kG1_LDA + kk];
-        const double b0 = b[kk * kG1_LDB + 16 * wn + (lane >> 2)];
-        const double b1 = b[kk * kG1_LDB + 16 * wn + 8 + (lane >> 2)];
-        dmma(acc[0][0][0], acc[0][0][1], a0, b0);
-        dmma(acc[0][1][0], acc[0][1][1], a0, b1);
-        dmma(acc[1][0][0], acc[1][0][1], a1, b0);
-        dmma(acc[1][1][0], acc[1][1][1], a1, b1);
+        for (int k4 = 0; k4 < kG1K / 4; ++k4) {
+          const int kl = 4 * k4 + kk;
+          double af[4], bf[2];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int ml = 32 * wm + 8 * mt + mm;
+            const double v = a[ml * kG1LDA + kl];
+            af[mt] = (diag && kb + kl > rb + ml) ? 0.0 : v;
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) bf[nt] = b[kl * kG1LDB + 16 * wn + 8 * nt + mm];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncthreads();
       }
-      __syncthreads();
-    }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int r = rb + 16 * wm + 8 * mt + (lane >> 2);
-      if (r >= s) continue;
+      for (int mt = 0; mt < 4; ++mt) {
+        const int r = rb + 32 * wm + 8 * mt + mm;
+        if (r >= s) continue;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int c = 16 * wn + 8 * nt + 2 * (lane & 3);
-        *reinterpret_cast<double2*>(Xg + (long long)r * kB + c) =
-            make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        for (int nt = 0; nt < 2; ++nt) {
+          const int c = 16 * wn + 8 * nt + 2 * kk;
+          *reinterpret_cast<double2*>(X + (long long)r * kB + c) =
+              make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        }
       }
     }
   }
   __syncthreads();
-}
-
-// ---- GEMM 2: A22 -= W2 V^T + V W2^T  (full symmetric storage) ------------
-// As A22 += Aop * Bop^T with Aop = -[W2 | V], Bop = [V | W2] (s x 2kB).
-__device__ void gemm2(double* A22, int ldw, int s, const double* W2g,
-                      const double* Vg, double* sm) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;
-  double* sOA = sm;
-  double* sOB[2] = {sm + kG2_OP, sm + 2 * kG2_OP};
-  const int ncb = (s + 63) / 64;
-  for (int rb = 0; rb < s; rb += 64) {
-    __syncthreads();
-    for (int t = tid; t < 64 * 2 * kB; t += kNT) {
-      const int r = t / (2 * kB), k = t % (2 * kB);
-      const int gr = rb + r;
-      double v = 0.0;
-      if (gr < s)
-        v = k < kB ? W2g[(long long)gr * kB + k] : Vg[(long long)gr * kB + k - kB];
-      sOA[r * kG2_LD + k] = -v;
-    }
-    auto stage = [&](int cb, int buf) {
-      for (int t = tid; t < 64 * 32; t += kNT) {
-        const int r = t >> 5, k2 = (t & 31) * 2;
-        const int gr = cb + r;
-        const int bytes = gr < s ? 16 : 0;
-        const double* src =
-            k2 < kB ? Vg + (long long)(bytes ? gr : 0) * kB + k2
-                    : W2g + (long long)(bytes ? gr : 0) * kB + (k2 - kB);
-        cp_async16(sOB[buf] + r * kG2_LD + k2, src, bytes);
-      }
-      cpa_commit();
-    };
-    stage(0, 0);
-    for (int ci = 0; ci < ncb; ++ci) {
-      const int cb = ci * 64;
-      // C fragments straight from global (issued before the wait)
+  // ---------------- pass 2
+  {
+    double* sA[2] = {sm, sm + kG1_T};
+    double* sB[2] = {sm + 2 * kG1_T, sm + 2 * kG1_T + kG1_B};
+    for (int cb = 0; cb < s; cb += kG1M) {
+      const int k0 = cb + 1;  // rows r > c >= cb
+      if (k0 >= s) break;
+      const int nk = (s - k0 + kG1K - 1) / kG1K;
       double acc[4][2][2];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const int r = rb + 32 * wm + 8 * mt + (lane >> 2);
+        const int r = cb + 32 * wm + 8 * mt + mm;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
-          const int c = cb + 16 * wn + 8 * nt + 2 * (lane & 3);
-          if (r < s && c < s) {
-            const double* p = A22 + (long long)r * ldw + c;
-            acc[mt][nt][0] = p[0];
-            acc[mt][nt][1] = (c + 1 < s) ? p[1] : 0.0;
+          const int c = 16 * wn + 8 * nt + 2 * kk;
+          if (r < s) {
+            const double2 x = *reinterpret_cast<const double2*>(X + (long long)r * kB + c);
+            acc[mt][nt][0] = x.x;
+            acc[mt][nt][1] = x.y;
           } else {
             acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
           }
         }
       }
+      const int cend = min(cb + kG1M, s);
+      auto stage = [&](int kb, int buf) {
+        for (int t = tid; t < kG1K * (kG1M / 2); t += kNT) {
+          const int r = t >> 6, c2 = (t & 63) * 2;
+          const int gr = kb + r, gc = cb + c2;
+          int bytes = 0;
+          if (gr < s && gc < cend) bytes = (gc + 1 < cend) ? 16 : 8;
+          cp_async16(sA[buf] + r * kG1TLD + c2,
+                     bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
+        }
+        for (int t = tid; t < kG1K * (kB / 2); t += kNT) {
+          const int r = t >> 4, c2 = (t & 15) * 2;
+          const int gr = kb + r;
+          const int bytes = gr < s ? 16 : 0;
+          cp_async16(sB[buf] + r * kG1LDB + c2,
+                     bytes ? VT + (long long)gr * kB + c2 : VT, bytes);
+        }
+        cpa_commit();
+      };
+      __syncthreads();
+      stage(k0, 0);
+      for (int ki = 0; ki < nk; ++ki) {
+        if (ki + 1 < nk) {
+          stage(k0 + (ki + 1) * kG1K, (ki + 1) & 1);
+          cpa_wait1();
+        } else {
+          cpa_wait0();
+        }
+        __syncthreads();
+        const double* a = sA[ki & 1];
+        const double* b = sB[ki & 1];
+        const int kb = k0 + ki * kG1K;
+        const bool diag = kb < cb + kG1M;
+#pragma unroll
+        for (int k4 = 0; k4 < kG1K / 4; ++k4) {
+          const int kl = 4 * k4 + kk;
+          double af[4], bf[2];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int ml = 32 * wm + 8 * mt + mm;
+            const double v = a[kl * kG1TLD + ml];
+            af[mt] = (diag && kb + kl <= cb + ml) ? 0.0 : v;
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) bf[nt] = b[kl * kG1LDB + 16 * wn + 8 * nt + mm];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int r = cb + 32 * wm + 8 * mt + mm;
+        if (r >= s) continue;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int c = 16 * wn + 8 * nt + 2 * kk;
+          *reinterpret_cast<double2*>(X + (long long)r * kB + c) =
+              make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---- GEMM 2: A22 -= W2 V^T + V W2^T on the lower triangle ----------------
+// As A22 += Aop Bop^T, Aop = -[W2 | V], Bop = [V | W2] (s x 2kB).  Row blocks
+// of 128 (Aop staged once), column blocks of 64 up to the diagonal (Bop
+// double-buffered by cp.async), C tiles prefetched into registers one tile
+// ahead.  Tiles crossing the diagonal also write their (never read) upper
+// part.
+__device__ void gemm2(double* A22, int ldw, int s, const double* W2,
+                      const double* V, double* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = lane & 3, mm = lane >> 2;
+  const int wm = warp >> 1, wn = warp & 1;
+  double* sOA = sm;
+  double* sOB[2] = {sm + kG2_A, sm + kG2_A + kG2_B};
+  auto load_c = [&](int rb, int cb, double (&c)[4][4][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int r = rb + 32 * wm + 8 * mt + mm;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int col = cb + 32 * wn + 8 * nt + 2 * kk;
+        if (r < s && col + 1 < s) {
+          const double2 x =
+              *reinterpret_cast<const double2*>(A22 + (long long)r * ldw + col);
+          c[mt][nt][0] = x.x;
+          c[mt][nt][1] = x.y;
+        } else {
+          c[mt][nt][0] = (r < s && col < s) ? A22[(long long)r * ldw + col] : 0.0;
+          c[mt][nt][1] = 0.0;
+        }
+      }
+    }
+  };
+  auto stage_b = [&](int cb, int buf) {
+    for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
+      const int r = t >> 5, k2 = (t & 31) * 2;
+      const int gr = cb + r;
+      const int bytes = gr < s ? 16 : 0;
+      const double* src = k2 < kB ? V + (long long)(bytes ? gr : 0) * kB + k2
+                                  : W2 + (long long)(bytes ? gr : 0) * kB + (k2 - kB);
+      cp_async16(sOB[buf] + r * kG2LD + k2, src, bytes);
+    }
+    cpa_commit();
+  };
+  for (int rb = 0; rb < s; rb += kG2M) {
+    __syncthreads();
+    for (int t = tid; t < kG2M * kG2K; t += kNT) {
+      const int r = t / kG2K, k = t % kG2K;
+      const int gr = rb + r;
+      double v = 0.0;
+      if (gr < s) v = k < kB ? W2[(long long)gr * kB + k] : V[(long long)gr * kB + k - kB];
+      sOA[r * kG2LD + k] = -v;
+    }
+    const int cend = min(rb + kG2M, s);
+    const int ncb = (cend + kG2N - 1) / kG2N;
+    double cn[4][4][2];
+    load_c(rb, 0, cn);
+    stage_b(0, 0);
+    for (int ci = 0; ci < ncb; ++ci) {
+      const int cb = ci * kG2N;
+      double acc[4][4][2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          acc[mt][nt][0] = cn[mt][nt][0];
+          acc[mt][nt][1] = cn[mt][nt][1];
+        }
       if (ci + 1 < ncb) {
-        stage(cb + 64, (ci + 1) & 1);
+        load_c(rb, cb + kG2N, cn);
+        stage_b(cb + kG2N, (ci + 1) & 1);
         cpa_wait1();
       } else {
         cpa_wait0();
@@ -365,32 +682,31 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2g,
       __syncthreads();
       const double* b = sOB[ci & 1];
 #pragma unroll 4
-      for (int k4 = 0; k4 < 2 * kB / 4; ++k4) {
-        const int kk = 4 * k4 + (lane & 3);
-        double af[4], bf[2];
+      for (int k4 = 0; k4 < kG2K / 4; ++k4) {
+        const int kl = 4 * k4 + kk;
+        double af[4], bf[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[mt] = sOA[(32 * wm + 8 * mt + mm) * kG2LD + kl];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bf[nt] = b[(32 * wn + 8 * nt + mm) * kG2LD + kl];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
-          af[mt] = sOA[(32 * wm + 8 * mt + (lane >> 2)) * kG2_LD + kk];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-          bf[nt] = b[(16 * wn + 8 * nt + (lane >> 2)) * kG2_LD + kk];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
+          for (int nt = 0; nt < 4; ++nt)
             dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
       }
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const int r = rb + 32 * wm + 8 * mt + (lane >> 2);
+        const int r = rb + 32 * wm + 8 * mt + mm;
         if (r >= s) continue;
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int c = cb + 16 * wn + 8 * nt + 2 * (lane & 3);
-          if (c >= s) continue;
-          double* p = A22 + (long long)r * ldw + c;
-          p[0] = acc[mt][nt][0];
-          if (c + 1 < s) p[1] = acc[mt][nt][1];
+        for (int nt = 0; nt < 4; ++nt) {
+          const int col = cb + 32 * wn + 8 * nt + 2 * kk;
+          double* p = A22 + (long long)r * ldw + col;
+          if (col + 1 < s)
+            *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          else if (col < s)
+            p[0] = acc[mt][nt][0];
         }
       }
       __syncthreads();
@@ -415,9 +731,14 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
   double* sT = smem + kGemmSmem;
   double* sG = sT + kSmallMat;   // G, then Y
   double* sM = sG + kSmallMat;
-  double* red = sM + kSmallMat;  // 8 + 8*kB
-  double* stau = red + 8 + 8 * kB;
+  double* sA = sM + kSmallMat;
+  double* sB = sA + kSmallMat;
+  double* sR = sB + kSmallMat;
+  double* red = sR + kSmallMat;
+  double* stau = red + kRed;
   double* wsm = stau + kB;
+  double* sS = wsm + kB;
+  int* sflag = reinterpret_cast<int*>(sS + kB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = args.n, ldw = args.ldw;
   double* W = args.ws + blockIdx.x * args.ws_stride;
@@ -429,12 +750,22 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
     const int j = args.js[sidx];
     const int m = j < 0 ? n : n - 1;
     double* band = args.band + sidx * args.band_stride;
-    // materialise the minor (index remap r' = r + (r >= j)), full storage
+    // materialise the lower triangle of the minor (r' = r + (r >= j))
     for (int r = warp; r < m; r += kNT / 32) {
       const int rr = (j >= 0 && r >= j) ? r + 1 : r;
       const double* src = args.A + (long long)rr * n;
       double* dst = W + (long long)r * ldw;
-      for (int c = lane; c < m; c += 32) dst[c] = src[(j >= 0 && c >= j) ? c + 1 : c];
+      for (int c0 = lane; c0 <= r; c0 += 128) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = c0 + 32 * u;
+          v[u] = cc <= r ? src[(j >= 0 && cc >= j) ? cc + 1 : cc] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + 32 * u <= r) dst[c0 + 32 * u] = v[u];
+      }
     }
     __syncthreads();
     int c = 0;
@@ -442,37 +773,42 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
       const int s = m - c - kB;
       if (s < 2) break;
       const int c0 = c + kB;
-      panel_qr(W, ldw, c0, c, s, Vg, stau, red, wsm);
-      write_band(W, ldw, m, c, c + kB, band);
-      // T (dlarft, forward columnwise) from G = V^T V
-      gram(Vg, Vg, s, sG, sgemm);
-      if (warp == 0) {
-        for (int t = 0; t < kB; ++t) {
-          // column t: T[q][t] = -tau_t * sum_{p=q}^{t-1} T[q][p] G[p][t]
-          double v = 0.0;
-          if (lane < t)
-            for (int p = lane; p < t; ++p) v += sT[lane * kSmallLD + p] * sG[p * kSmallLD + t];
-          __syncwarp();
-          if (lane < t) sT[lane * kSmallLD + t] = -stau[t] * v;
-          if (lane == t) sT[t * kSmallLD + t] = stau[t];
-          if (lane > t) sT[lane * kSmallLD + t] = 0.0;
-          __syncwarp();
+      double* P0 = W + (long long)c0 * ldw + c;
+      const bool fast = s >= 2 * kB &&
+                        chol_panel(P0, ldw, s, Vg, Xg, sT, sG, sA, sB, sR, sS,
+                                   sgemm, sflag);
+      if (!fast) {
+        panel_qr(P0, ldw, s, stau, red, wsm);
+        extract_v(P0, ldw, s, Vg);
+        // T (dlarft, forward columnwise) from G = V^T V
+        gram(Vg, kB, Vg, kB, s, sG, sgemm);
+        if (warp == 0) {
+          for (int t = 0; t < kB; ++t) {
+            double v = 0.0;
+            if (lane < t)
+              for (int p = lane; p < t; ++p) v += sT[lane * kSmallLD + p] * sG[p * kSmallLD + t];
+            __syncwarp();
+            if (lane < t) sT[lane * kSmallLD + t] = -stau[t] * v;
+            if (lane == t) sT[t * kSmallLD + t] = stau[t];
+            if (lane > t) sT[lane * kSmallLD + t] = 0.0;
+            __syncwarp();
+          }
         }
       }
       __syncthreads();
-      row_transform(Vg, sT, 1.0, nullptr, VTg, s);           // VT = V T
+      write_band(W, ldw, m, c, c + kB, band);
+      row_transform(Vg, kB, sT, 1.0, nullptr, VTg, s);       // VT = V T
       double* A22 = W + (long long)c0 * ldw + c0;
       gemm1(A22, ldw, s, VTg, Xg, sgemm);                     // X = A22 VT
-      gram(Vg, Xg, s, sG, sgemm);                             // Y = V^T X
-      // M = T^T Y
-      for (int t = tid; t < kB * kB; t += kNT) {
+      gram(Vg, kB, Xg, kB, s, sG, sgemm);                     // Y = V^T X
+      for (int t = tid; t < kB * kB; t += kNT) {              // M = T^T Y
         const int q = t / kB, p = t % kB;
         double v = 0.0;
         for (int u = 0; u <= q; ++u) v += sT[u * kSmallLD + q] * sG[u * kSmallLD + p];
         sM[q * kSmallLD + p] = v;
       }
       __syncthreads();
-      row_transform(Vg, sM, -0.5, Xg, Xg, s);                 // W2 = X - V M/2
+      row_transform(Vg, kB, sM, -0.5, Xg, Xg, s);             // W2 = X - V M/2
       gemm2(A22, ldw, s, Xg, Vg, sgemm);                      // A22 -= W2V^T+VW2^T
     }
     write_band(W, ldw, m, c, m, band);
