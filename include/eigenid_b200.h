@@ -154,6 +154,14 @@ int eigenid_gpu_c5_mu_device(eigenid_gpu_ctx* ctx, uint64_t seed,
  * bench's gpu_launches field). */
 uint64_t eigenid_gpu_launch_count(eigenid_gpu_ctx* ctx);
 
+/* Per-stage device timing of the large-n pipeline (CUDA events on the
+ * context stream): stage1 (dense->band), stage2 (bulge chase), bisection of
+ * lambda(A), bisection of the minors, identity.  Off by default. */
+void eigenid_gpu_set_profiling(eigenid_gpu_ctx* ctx, int on);
+/* Copies up to `cap` stage times (ms) of the last large-n call; returns the
+ * count written. */
+int eigenid_gpu_stage_times(eigenid_gpu_ctx* ctx, double* ms, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,8 @@ SIGNATURES = {
                                            C.c_size_t, C.c_size_t, C.c_size_t,
                                            C.c_void_p, C.POINTER(GpuErr)]),
     "eigenid_gpu_launch_count": (C.c_uint64, [C.c_void_p]),
+    "eigenid_gpu_set_profiling": (None, [C.c_void_p, C.c_int]),
+    "eigenid_gpu_stage_times": (C.c_int, [C.c_void_p, _dp, C.c_int]),
 }
 
 _lib = None

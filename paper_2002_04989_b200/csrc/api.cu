@@ -151,6 +151,8 @@ struct eigenid_gpu_ctx {
       bE2, bAe, bJs, bTmpOut, bTmpMu;
   std::atomic<size_t> solves{0};
   std::atomic<uint64_t> launches{0};
+  bool profiling = false;
+  double stage_ms[5] = {0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -249,35 +251,42 @@ int begin(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
   return EIGENID_OK;
 }
 
-// EIGENID_PROFILE=1 prints per-stage device times of run_large to stderr
-// (development aid; the bench times whole steps with its own events).
+// Per-stage device timing of run_large: enabled per context through
+// eigenid_gpu_set_profiling (bench.py reads it to time the stage-1 kernel on
+// its own stream) or EIGENID_PROFILE=1 (also printed to stderr).
+constexpr int kStages = 5;  // stage1, stage2, bisect_A, bisect_minors, identity
 struct StageTimer {
-  bool on = false;
+  bool on = false, print = false;
   cudaStream_t st = nullptr;
-  std::vector<cudaEvent_t> ev;
-  std::vector<const char*> names;
-  explicit StageTimer(cudaStream_t s) : st(s) {
+  cudaEvent_t ev[kStages + 1];
+  int slot[kStages + 1];
+  int count = 0;
+  double* sink = nullptr;  // ctx->stage_ms
+  StageTimer(cudaStream_t s, bool enabled, double* out) : st(s), sink(out) {
     const char* e = std::getenv("EIGENID_PROFILE");
-    on = e && e[0] == '1';
-    mark("start");
+    print = e && e[0] == '1';
+    on = enabled || print;
+    mark(-1);
   }
-  void mark(const char* name) {
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    ev.push_back(e);
-    names.push_back(name);
+  void mark(int stage) {
+    if (!on || count > kStages) return;
+    cudaEventCreate(&ev[count]);
+    cudaEventRecord(ev[count], st);
+    slot[count++] = stage;
   }
   ~StageTimer() {
     if (!on) return;
-    cudaEventSynchronize(ev.back());
-    for (size_t t = 1; t < ev.size(); ++t) {
+    static const char* names[kStages] = {"stage1", "stage2", "bisect_A",
+                                         "bisect_minors", "identity"};
+    cudaEventSynchronize(ev[count - 1]);
+    for (int t = 0; t < kStages; ++t) sink[t] = 0.0;
+    for (int t = 1; t < count; ++t) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[t - 1], ev[t]);
-      std::fprintf(stderr, "[eigenid] %-14s %10.3f ms\n", names[t], ms);
+      sink[slot[t]] = ms;
+      if (print) std::fprintf(stderr, "[eigenid] %-14s %10.3f ms\n", names[slot[t]], ms);
     }
-    for (auto e : ev) cudaEventDestroy(e);
+    for (int t = 0; t < count; ++t) cudaEventDestroy(ev[t]);
   }
 };
 
@@ -306,22 +315,22 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   solve_list_kernel<<<(nsolves + 255) / 256, 256, 0, st>>>(djs, j0, rows);
   ++launches;
 
-  StageTimer timer(st);
+  StageTimer timer(st, c->profiling, c->stage_ms);
   Stage1Args s1{dA, n, djs, nsolves, c->bWs.as<double>(), ws_stride, ldw,
                 c->bBand.as<double>(), band_stride};
   EID_CUDA(launch_stage1(s1, slots, st), "stage1");
-  timer.mark("stage1");
+  timer.mark(0);
   ++launches;
   Stage2Args s2{c->bBand.as<double>(), band_stride, djs, nsolves, n,
                 c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(), n};
   EID_CUDA(launch_stage2(s2, st), "stage2");
   ++launches;
-  timer.mark("stage2");
+  timer.mark(1);
   // lambda(A): Gershgorin brackets, split across CTAs
   BisectArgs ba{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
                 n, djs, nsolves, 0, n, nullptr, dlam, n, (n + 255) / 256};
   EID_CUDA(launch_bisect(ba, 1, n, st, &launches), "bisect A");
-  timer.mark("bisect_A");
+  timer.mark(2);
   if (identity) EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol,
                                            c->dstatus, st, &launches),
                          "degeneracy");
@@ -329,7 +338,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
     BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
                   n, djs, nsolves, 1, n, dlam, dmu, n - 1, 1};
     EID_CUDA(launch_bisect(bm, rows, n - 1, st, &launches), "bisect minors");
-    timer.mark("bisect_minors");
+    timer.mark(3);
   }
   if (identity && rows > 0) {
     const int batch = batch_of(cfg, n);
@@ -345,7 +354,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
                              c->bFlags.as<long long>(), cap, c->dstatus,
                              cfg->log_domain, st, &launches),
              "identity");
-    timer.mark("identity");
+    timer.mark(4);
   }
   c->launches += launches;
   return EIGENID_OK;
@@ -483,6 +492,15 @@ int eigenid_gpu_sync(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
 size_t eigenid_gpu_solve_count(eigenid_gpu_ctx* c) { return c->solves.load(); }
 void eigenid_gpu_reset_solve_count(eigenid_gpu_ctx* c) { c->solves.store(0); }
 uint64_t eigenid_gpu_launch_count(eigenid_gpu_ctx* c) { return c->launches.load(); }
+
+void eigenid_gpu_set_profiling(eigenid_gpu_ctx* c, int on) { c->profiling = on != 0; }
+
+int eigenid_gpu_stage_times(eigenid_gpu_ctx* c, double* ms, int cap) {
+  std::lock_guard<std::mutex> g(c->mu);
+  const int k = cap < 5 ? cap : 5;
+  for (int t = 0; t < k; ++t) ms[t] = c->stage_ms[t];
+  return k;
+}
 
 int eigenid_gpu_eigenvalues(eigenid_gpu_ctx* c, const double* a, size_t n,
                             double* out, eigenid_gpu_err* err) {

@@ -159,6 +159,16 @@ class Device:
         err = _native.GpuErr()
         _native.check(self.lib.eigenid_gpu_sync(self.ctx, C.byref(err)), err)
 
+    def set_profiling(self, on: bool) -> None:
+        self.lib.eigenid_gpu_set_profiling(self.ctx, 1 if on else 0)
+
+    def stage_times(self) -> dict:
+        """ms per stage of the last large-n call (needs set_profiling)."""
+        buf = (C.c_double * 5)()
+        k = self.lib.eigenid_gpu_stage_times(self.ctx, buf, 5)
+        names = ["stage1", "stage2", "bisect_A", "bisect_minors", "identity"]
+        return {names[t]: buf[t] for t in range(k)}
+
     def __del__(self):
         try:
             if self.ctx:
