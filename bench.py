@@ -323,6 +323,7 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
     import torch
 
     from paper_2002_04989_b200 import IdentityConfig, IdentityEngine
+    from paper_2002_04989_b200.shard import gather_rows, shard_range
     torch.cuda.set_device(dist.local)
     eng = IdentityEngine(IdentityConfig(), device=dist.local)
     dev = eng.device
@@ -338,26 +339,27 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
                   .random_symmetric(1, 64),
                   "C3": lambda: c3_matrix(1024), "C4": lambda: goe_matrix(4096)}[wl]()
         a_dev = torch.from_numpy(a_host).to(f"cuda:{dist.local}")
-        j0, j1 = rank * n // world, (rank + 1) * n // world
+        j0, j1 = shard_range(n, world, rank)
         rows = j1 - j0
         out_dev = torch.empty((rows, n), dtype=torch.float64, device=a_dev.device)
         lam_dev = torch.empty(n, dtype=torch.float64, device=a_dev.device)
         mu_dev = torch.empty((max(rows, 1), n - 1), dtype=torch.float64, device=a_dev.device)
-        full = torch.empty((n, n), dtype=torch.float64, device=a_dev.device) if world > 1 else None
+        full = None
         units = n * n
 
         def step():
+            nonlocal full
             eng.all_magnitudes_device(a_dev.data_ptr(), n, j0, j1, out_dev.data_ptr(),
                                       lam_dev.data_ptr(), mu_dev.data_ptr())
             if world > 1:
                 with torch.cuda.stream(stream):
-                    dist.pg.all_gather_into_tensor(full, out_dev)
+                    full = gather_rows(out_dev, n, world, dist.pg)
         flops = f_tri(n, rows) + f_id(n, rows)
     elif wl == "C2":
         from oracle.oracle import Oracle
         orc = Oracle()
         count = 4096
-        b0, b1 = rank * count // world, (rank + 1) * count // world
+        b0, b1 = shard_range(count, world, rank)
         a_host = np.stack([orc.random_symmetric(b, 32) for b in range(b0, b1)])
         a_dev = torch.from_numpy(a_host).to(f"cuda:{dist.local}")
         out_dev = torch.empty((b1 - b0, 32 * 32), dtype=torch.float64, device=a_dev.device)
@@ -372,7 +374,7 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
         orc = Oracle()
         lam_host = orc.c5_lambda(5, n)
         lam_dev = torch.from_numpy(lam_host).to(f"cuda:{dist.local}")
-        j0, j1 = rank * n // world, (rank + 1) * n // world
+        j0, j1 = shard_range(n, world, rank)
         rows = j1 - j0
         mu_dev = torch.empty((rows, n - 1), dtype=torch.float64, device=lam_dev.device)
         eng.c5_mu_device(5, lam_dev.data_ptr(), n, j0, j1, mu_dev.data_ptr())

@@ -93,10 +93,12 @@ cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
 
 __global__ void init_status_kernel(DevStatus* st) {
   st[0].code = 0;
+  st[0].phase = 0;
   st[0].index = -1;
   st[0].gap = 0.0;
   st[0].aux = -1;
   st[1].code = 0;
+  st[1].phase = 0;
   st[1].index = -1;  // == ULLONG_MAX for the atomicMin in degeneracy_kernel
   st[1].gap = 0.0;
   st[1].aux = -1;
@@ -216,8 +218,7 @@ int finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
   char buf[200];
   switch (s.code) {
     case EIGENID_E_DEGENERATE:
-      if (s.index >= 0 && s.aux < 0 && s.gap >= 0.0 && degenerate)
-        *degenerate = true;
+      if (s.phase == 1 && degenerate) *degenerate = true;
       if (s.aux >= 0)
         std::snprintf(buf, sizeof buf,
                       "spectrum is degenerate between eigenvalues %lld and %lld"

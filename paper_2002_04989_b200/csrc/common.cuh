@@ -16,7 +16,7 @@ constexpr double kSafeMin = 2.2250738585072014e-308;   // DBL_MIN
 // Per-solve / per-call device status record (reduced with atomics).
 struct DevStatus {
   int code;        // eigenid_status
-  int pad;
+  int phase;       // 1: lambda(A) degeneracy check (identity.cpp:141-149)
   long long index; // eigenvalue index (degeneracy) / component index
   double gap;
   long long aux;   // matrix index (batched) or output row
@@ -44,11 +44,12 @@ __device__ __forceinline__ double warp_min(double v) {
 // enough for reporting; any error aborts the call on the host side).
 __device__ __forceinline__ void set_status(DevStatus* st, int code,
                                            long long index, double gap,
-                                           long long aux = -1) {
+                                           long long aux = -1, int phase = 0) {
   if (atomicCAS(&st->code, 0, code) == 0) {
     st->index = index;
     st->gap = gap;
     st->aux = aux;
+    st->phase = phase;
   }
 }
 

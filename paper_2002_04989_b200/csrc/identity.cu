@@ -244,6 +244,7 @@ __global__ void degeneracy_finish_kernel(const double* __restrict__ lam,
   if (status[1].code == 2 && status[0].code == 0) {
     const long long k = status[1].index;
     status[0].code = 2;
+    status[0].phase = 1;
     status[0].index = k;
     status[0].gap = lam[k + 1] - lam[k];
   }

@@ -181,7 +181,7 @@ __global__ void small_all_magnitudes_kernel(const double* __restrict__ A,
     const double range = lam[n - 1] - lam[0];
     for (int k = 0; k + 1 < n; ++k)
       if (lam[k + 1] - lam[k] <= tol * range) {
-        set_status(status, 2, k, lam[k + 1] - lam[k], mat);
+        set_status(status, 2, k, lam[k + 1] - lam[k], mat, 1);
         degenerate = 1;
         break;
       }

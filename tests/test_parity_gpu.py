@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle.
+
+Tolerances (stated here):
+  * full pipeline (different eigensolvers on each side): elementwise
+    |g - c| <= 1e-9 |c| + 1e-12 — the reference's own QL-vs-Jacobi spread
+    rules out a pure relative bound on tiny entries;
+  * identity stage on identical spectra: bit-exact (the kernel keeps the
+    reference's pairing, batching and combine order);
+  * full-size configs C3/C4/C5: size-independent properties (doubly
+    stochastic, interlacing, trace, [0,1] range, shard/batch invariance)
+    plus sampled bit-exact components.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def mixed_ok(g, c, rel=1e-9, abs_=1e-12):
+    return float(np.max(np.abs(g - c) - (rel * np.abs(c) + abs_))) <= 0.0
+
+
+def bits(x):
+    return np.ascontiguousarray(x, np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def gold():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+
+
+# ------------------------------------------------------------- small / fused
+def test_acceptance_oracle_equivalence_small(engine, oracle):
+    """acceptance.cpp:54-73: 100 seeded matrices, n = 2..64 (fused kernel)."""
+    for t in range(100):
+        n = 2 + t % 63
+        a = oracle.random_symmetric(1000 + t, n)
+        g = engine.all_magnitudes(a).reshape(n, n)
+        c, lam, mu = oracle.all_magnitudes(a, return_spectra=True)
+        assert mixed_ok(g, c), (t, n, float(np.max(np.abs(g - c))))
+        assert np.max(np.abs(g - c)) <= 1e-8  # the acceptance bound itself
+
+
+def test_golden_reference_vectors(engine, gold):
+    for seed, n in gold["cases"]:
+        key = f"s{seed}_n{n}"
+        g, lam, _ = engine.all_magnitudes(gold[f"{key}_a"], return_spectra=True)
+        assert mixed_ok(g.reshape(n, n), gold[f"{key}_all64"]), key
+        assert np.max(np.abs(lam - gold[f"{key}_lam"])) <= 1e-13 * max(1, n)
+
+
+def test_identity_stage_bit_exact_all_batch_sizes(oracle):
+    from paper_2002_04989_b200 import IdentityConfig, IdentityEngine
+    for n, seed in ((17, 3), (64, 4), (130, 5), (301, 6)):
+        a = oracle.random_symmetric(seed, n)
+        _, lam, mu = oracle.all_magnitudes(a, return_spectra=True)
+        for b in (1, 7, 64, n - 1, n + 5):
+            want = oracle.identity_rows(lam, mu, batch=b)
+            got = IdentityEngine(IdentityConfig(batch_size=b)).identity(lam, mu)
+            # bit-exact wherever the reference's batched product is finite;
+            # entries that overflow a batch take the log-domain retry, where
+            # device log/exp may differ from glibc in the last ulps
+            for j, i in zip(*np.nonzero(bits(got) != bits(want))):
+                v, raw, method = oracle.evaluate(lam, mu[j], int(i), batch=b)
+                assert method == 3, (n, b, j, i)
+                assert abs(got[j, i] - want[j, i]) <= 1e-12 * abs(want[j, i]), (n, b, j, i)
+
+
+def test_log_domain_evaluation(oracle):
+    from paper_2002_04989_b200 import IdentityConfig, IdentityEngine
+    a = oracle.random_symmetric(21, 40)
+    _, lam, mu = oracle.all_magnitudes(a, return_spectra=True)
+    want = oracle.identity_rows(lam, mu, log_domain=True)
+    got = IdentityEngine(IdentityConfig(evaluation="log-domain")).identity(lam, mu)
+    # device log/exp vs glibc: within a few ulps, not bit-exact
+    assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)) <= 1e-12
+    full = IdentityEngine(IdentityConfig(evaluation="log-domain")).all_magnitudes(a)
+    assert mixed_ok(full.reshape(40, 40), oracle.all_magnitudes(a, log_domain=True))
+
+
+# ------------------------------------------------------------- large / two-stage
+@pytest.mark.parametrize("n", [65, 66, 97, 128, 129, 200, 257, 300])
+def test_two_stage_pipeline_vs_oracle(engine, oracle, n):
+    a = oracle.random_symmetric(500 + n, n)
+    g, lam, mu = engine.all_magnitudes(a, return_spectra=True)
+    c, lc, mc = oracle.all_magnitudes(a, return_spectra=True)
+    assert mixed_ok(g.reshape(n, n), c), float(np.max(np.abs(g.reshape(n, n) - c)))
+    assert np.max(np.abs(lam - lc)) <= 1e-13 * n
+    assert np.max(np.abs(mu - mc)) <= 1e-13 * n
+    # identity stage on the GPU's own spectra reproduces the oracle bit-exact
+    assert np.array_equal(bits(g.reshape(n, n)), bits(oracle.identity_rows(lam, mu)))
+
+
+def test_eigenvalues_entry(oracle):
+    from paper_2002_04989_b200 import eigenvalues
+    for n in (1, 2, 3, 31, 64, 65, 200, 513):
+        a = oracle.random_symmetric(n, n)
+        assert np.max(np.abs(eigenvalues(a) - oracle.eigenvalues(a))) <= 1e-13 * max(n, 1)
+
+
+def test_hand_cases_and_errors(engine, gold):
+    import paper_2002_04989_b200 as eid
+    assert np.allclose(engine.all_magnitudes(np.array([[2.0, 1.0], [1.0, 2.0]])), 0.5,
+                       atol=1e-12, rtol=0)
+    assert np.allclose(engine.all_magnitudes(np.diag([1.0, 2.0, 3.0])).reshape(3, 3),
+                       np.eye(3), atol=1e-12)
+    blk = np.array([[2.0, 1.0, 0.0], [1.0, 2.0, 0.0], [0.0, 0.0, 10.0]])
+    g = engine.all_magnitudes(blk).reshape(3, 3)
+    assert g[2, 0] <= 1e-8 and g[0, 2] <= 1e-8
+    assert mixed_ok(g, gold["hand_block"], abs_=1e-12)
+    with pytest.raises(eid.DegenerateEigenvalue):
+        engine.all_magnitudes(np.eye(5))
+    with pytest.raises(eid.DegenerateEigenvalue):
+        engine.all_magnitudes(np.eye(80))        # two-stage path
+    with pytest.raises(eid.MatrixTooSmall):
+        engine.all_magnitudes(np.eye(1))
+
+
+def test_solve_count_contract(oracle):
+    from paper_2002_04989_b200 import IdentityEngine
+    eng = IdentityEngine()
+    for n in (14, 90):
+        eng.reset_solve_count()
+        eng.all_magnitudes(oracle.random_symmetric(6, n))
+        assert eng.eigenvalue_solve_count() == n + 1
+    eng.reset_solve_count()
+    with pytest.raises(Exception):
+        eng.all_magnitudes(np.eye(5))
+    assert eng.eigenvalue_solve_count() == 1  # lambda(A) solved, then degenerate
+
+
+def test_overflow_robustness(engine, oracle, gold):
+    """test_identity.cpp:284-296: n = 300 scaled 1e3 stays finite."""
+    a = oracle.random_symmetric(1, 300) * 1e3
+    g = engine.all_magnitudes(a).reshape(300, 300)
+    assert np.all(np.isfinite(g))
+    assert np.all((g >= 0) & (g <= 1))
+    assert mixed_ok(g, gold["ovf_all"], abs_=1e-11)
+
+
+def test_range_and_doubly_stochastic(engine, oracle):
+    for n in (32, 100, 257):
+        g = engine.all_magnitudes(oracle.random_symmetric(14, n)).reshape(n, n)
+        assert np.all((g >= 0) & (g <= 1))
+        assert np.max(np.abs(g.sum(0) - 1)) <= 1e-8
+        assert np.max(np.abs(g.sum(1) - 1)) <= 1e-8
+
+
+def test_determinism_and_shard_invariance(engine, oracle):
+    """Bit-identical across repeated calls and across j-shards (the GPU form
+    of test_identity.cpp:130-143)."""
+    import torch
+    n = 150
+    a = oracle.random_symmetric(31, n)
+    g1 = engine.all_magnitudes(a)
+    g2 = engine.all_magnitudes(a)
+    assert np.array_equal(bits(g1), bits(g2))
+    dev = torch.from_numpy(a).cuda()
+    for (j0, j1) in ((0, 75), (75, 150), (10, 11), (149, 150)):
+        out = torch.empty((j1 - j0, n), dtype=torch.float64, device="cuda")
+        engine.all_magnitudes_device(dev.data_ptr(), n, j0, j1, out.data_ptr())
+        engine.sync()
+        assert np.array_equal(bits(out.cpu().numpy()), bits(g1.reshape(n, n)[j0:j1]))
+
+
+# ------------------------------------------------------------- configs
+def test_c1_n64(engine, oracle, gold):
+    a = oracle.random_symmetric(1, 64)
+    g = engine.all_magnitudes(a).reshape(64, 64)
+    assert mixed_ok(g, gold["s1_n64_all64"])
+
+
+def test_c2_batched_4096x32(engine, oracle):
+    mats = np.stack([oracle.random_symmetric(b, 32) for b in range(4096)])
+    got = engine.all_magnitudes_batched(mats).reshape(4096, 32, 32)
+    for b in range(0, 4096, 97):
+        assert mixed_ok(got[b], oracle.all_magnitudes(mats[b])), b
+    assert np.max(np.abs(got.sum(axis=2) - 1)) <= 1e-8
+    assert np.max(np.abs(got.sum(axis=1) - 1)) <= 1e-8
+
+
+def test_c3_prescribed_spectrum_n1024(engine, oracle):
+    import bench
+    a = bench.c3_matrix(1024)
+    g, lam, mu = engine.all_magnitudes(a, return_spectra=True)
+    g = g.reshape(1024, 1024)
+    prescribed = -1.0 + 2.0 * np.arange(1024) / 1023
+    assert np.max(np.abs(lam - prescribed)) <= 1e-13
+    assert np.max(np.abs(g.sum(0) - 1)) <= 1e-8 and np.max(np.abs(g.sum(1) - 1)) <= 1e-8
+    # sampled minors against the oracle eigensolver, then the rows exactly
+    rows = [0, 511, 1023]
+    for j in rows:
+        want = oracle.eigenvalues(oracle.minor(a, j))
+        assert np.max(np.abs(mu[j] - want)) <= 1e-13
+    assert np.array_equal(bits(g[rows]), bits(oracle.identity_rows(lam, mu[rows])))
+
+
+@pytest.mark.slow
+def test_c4_n4096_properties(engine):
+    import bench
+    a = bench.goe_matrix(4096)
+    g, lam, mu = engine.all_magnitudes(a, return_spectra=True)
+    g = g.reshape(4096, 4096)
+    assert np.all((g >= 0) & (g <= 1))
+    assert np.max(np.abs(g.sum(1) - 1)) <= 1e-10
+    assert np.max(np.abs(g.sum(0) - 1)) <= 1e-8
+    assert np.all(np.diff(lam) > 0) and np.all(np.diff(mu, axis=1) >= 0)
+    assert abs(lam.sum() - np.trace(a)) <= 1e-10
+    tol = 1e-11
+    assert np.all(mu >= lam[None, :-1] - tol) and np.all(mu <= lam[None, 1:] + tol)
+    for j in (0, 2047, 4095):  # trace of each minor
+        assert abs(mu[j].sum() - (np.trace(a) - a[j, j])) <= 1e-10
+
+
+def test_c5_identity_full_size(oracle):
+    """C5 at n = 32768 on one GPU: every row sums to one (Lagrange identity,
+    holds for any interlacing mu) and sampled components are bit-exact."""
+    import torch
+
+    from paper_2002_04989_b200 import IdentityEngine
+    n, rows = 32768, 64
+    eng = IdentityEngine()
+    lam = oracle.c5_lambda(5, n)
+    lam_d = torch.from_numpy(lam).cuda()
+    mu_d = torch.empty((rows, n - 1), dtype=torch.float64, device="cuda")
+    eng.c5_mu_device(5, lam_d.data_ptr(), n, 1000, 1000 + rows, mu_d.data_ptr())
+    out = torch.empty((rows, n), dtype=torch.float64, device="cuda")
+    eng.identity_device(lam_d.data_ptr(), mu_d.data_ptr(), n, 1000, 1000 + rows,
+                        out.data_ptr())
+    eng.sync()
+    mu = mu_d.cpu().numpy()
+    assert np.array_equal(bits(mu[:2]), bits(oracle.c5_mu_rows(5, lam, [1000, 1001])))
+    o = out.cpu().numpy()
+    assert np.max(np.abs(o.sum(1) - 1)) <= 1e-11
+    rng = np.random.default_rng(0)
+    for r, i in zip(rng.integers(0, rows, 12), rng.integers(0, n, 12)):
+        v, raw, _ = oracle.evaluate(lam, mu[r], int(i))
+        assert o[r, i] == v
+
+
+def test_c5_golden_rows(gold):
+    from paper_2002_04989_b200 import IdentityEngine
+    got = IdentityEngine().identity(gold["c5_lam_8192"], gold["c5_mu_8192"])
+    assert np.array_equal(bits(got), bits(gold["c5_id_8192"]))
