@@ -56,6 +56,12 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared",
               "-I" + os.path.join(ROOT, "include"), *hsrc, "-o", HOSTLIB,
               "-L" + PKG, "-leigenid_b200", "-Wl,-rpath,$ORIGIN", "-pthread"])
+    test_src = os.path.join(ROOT, "tests", "cpp", "test_host.cpp")
+    test_bin = os.path.join(ROOT, "tests", "cpp", "test_host")
+    if os.path.exists(test_src) and (force or _newer(test_bin, [test_src, HOSTLIB])):
+        _run(["g++", "-O2", "-std=c++17", "-I" + os.path.join(ROOT, "include"),
+              test_src, "-o", test_bin, "-L" + PKG, "-leigenid", "-leigenid_b200",
+              "-Wl,-rpath," + PKG, "-pthread"])
 
 
 if __name__ == "__main__":

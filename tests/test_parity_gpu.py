@@ -243,3 +243,15 @@ def test_c5_golden_rows(gold):
     from paper_2002_04989_b200 import IdentityEngine
     got = IdentityEngine().identity(gold["c5_lam_8192"], gold["c5_mu_8192"])
     assert np.array_equal(bits(got), bits(gold["c5_id_8192"]))
+
+
+def test_cpp_host_layer():
+    """The reference-shaped C++ API (include/eigenid/*.hpp) over the C-ABI."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "test_host")
+    if not os.path.exists(exe):
+        pytest.skip("C++ host test not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout
