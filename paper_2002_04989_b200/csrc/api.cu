@@ -71,6 +71,7 @@ struct Stage2Args {
   double* e2;
   double* ae;
   long long de_stride;
+  int* counter;
 };
 cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st);
 // bisect.cu
@@ -150,7 +151,7 @@ struct eigenid_gpu_ctx {
   DevStatus* dstatus = nullptr;
   DevStatus* hstatus = nullptr;  // pinned
   DevBuf bA, bOut, bLam, bMu, bDen, bRcp, bFlags, bFlagCount, bWs, bBand, bD,
-      bE2, bAe, bJs, bTmpOut, bTmpMu;
+      bE2, bAe, bJs, bTmpOut, bTmpMu, bCounter;
   std::atomic<size_t> solves{0};
   std::atomic<uint64_t> launches{0};
   bool profiling = false;
@@ -322,8 +323,10 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   EID_CUDA(launch_stage1(s1, slots, st), "stage1");
   timer.mark(0);
   ++launches;
+  EID_CUDA(c->bCounter.ensure(sizeof(int) * 4), "alloc counter");
   Stage2Args s2{c->bBand.as<double>(), band_stride, djs, nsolves, n,
-                c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(), n};
+                c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(), n,
+                c->bCounter.as<int>()};
   EID_CUDA(launch_stage2(s2, st), "stage2");
   ++launches;
   timer.mark(1);
@@ -474,7 +477,8 @@ int eigenid_gpu_destroy(eigenid_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->bA, &c->bOut, &c->bLam, &c->bMu, &c->bDen, &c->bRcp,
                     &c->bFlags, &c->bFlagCount, &c->bWs, &c->bBand, &c->bD,
-                    &c->bE2, &c->bAe, &c->bJs, &c->bTmpOut, &c->bTmpMu})
+                    &c->bE2, &c->bAe, &c->bJs, &c->bTmpOut, &c->bTmpMu,
+                    &c->bCounter})
     b->release();
   cudaFree(c->dstatus);
   cudaFreeHost(c->hstatus);

@@ -57,14 +57,11 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
   const double* gd = a.d + solve * a.de_stride;
   const double* ge2 = a.e2 + solve * a.de_stride;
   const double* gae = a.ae + solve * a.de_stride;
-  double glo = 1e308, ghi = -1e308, tn = 0.0, emax = 0.0;
+  double glo = 1e308, ghi = -1e308, tn = 0.0;
   for (int k = threadIdx.x; k < m; k += kBisNT) {
     const double dk = gd[k];
     sd[k] = dk;
-    if (k + 1 < m) {
-      se2[k] = ge2[k];
-      emax = fmax(emax, ge2[k]);
-    }
+    if (k + 1 < m) se2[k] = ge2[k];
     const double r = (k > 0 ? gae[k - 1] : 0.0) + (k + 1 < m ? gae[k] : 0.0);
     glo = fmin(glo, dk - r);
     ghi = fmax(ghi, dk + r);
@@ -73,13 +70,18 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
   glo = block_reduce_min(glo, red);
   ghi = block_reduce_max(ghi, red);
   tn = block_reduce_max(tn, red);
-  emax = block_reduce_max(emax, red);
-  const double pivmin = kSafeMin * fmax(1.0, emax);
-  const double fudge = 2.0 * kEps * tn * m + 2.0 * pivmin;
+  // exact power-of-two scaling to ||T|| <= 1 for the division-free count
+  const double sc = pow2_scale(tn);
+  for (int k = threadIdx.x; k < m; k += kBisNT) {
+    sd[k] *= sc;
+    if (k + 1 < m) se2[k] *= sc * sc;
+  }
+  __syncthreads();
+  const double fudge = 2.0 * kEps * tn * m + 1e-300;
   glo -= fudge;
   ghi += fudge;
-  const double atol = kEps * tn;
-  const double delta = 8.0 * (m + 1) * kEps * tn + pivmin;
+  const double atol = kEps * tn * sc;
+  const double delta = 8.0 * (m + 1) * kEps * tn;
   double* out = a.out + (long long)(solve - a.first_solve) * a.out_ld;
   const int per = (m + a.split - 1) / a.split;
   const int k0 = part * per, k1 = min(m, k0 + per);
@@ -87,8 +89,8 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
     double lo = glo, hi = ghi;
     if (a.lam) {
       const double l0 = a.lam[k] - delta, l1 = a.lam[k + 1] + delta;
-      if (sturm_count(sd, se2, m, l0, pivmin) <= k &&
-          sturm_count(sd, se2, m, l1, pivmin) > k) {
+      if (sturm_count(sd, se2, m, l0 * sc) <= k &&
+          sturm_count(sd, se2, m, l1 * sc) > k) {
         lo = fmax(l0, glo);
         hi = fmin(l1, ghi);
         if (!(lo < hi)) {
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
         }
       }
     }
-    out[k] = bisect_one(sd, se2, m, k, lo, hi, atol, pivmin);
+    out[k] = bisect_one(sd, se2, m, k, lo * sc, hi * sc, atol) / sc;
   }
   if (a.split > 1) return;  // cross-CTA order is checked by sort_fix_kernel
   __syncthreads();

@@ -4,23 +4,27 @@
 // Second half of the replacement for tridiagonalize (eigensolve.cpp:19-69).
 // Sweep st annihilates column st below the subdiagonal with a length-kB
 // reflector, then chases the bulge down the band block by block:
-//   right-apply the previous reflector to the off-diagonal block
-//   A[R', R], annihilate that block's first column with a new reflector,
-//   left-apply it to the rest of the block, two-sided apply it to the
-//   diagonal block A[R', R'].
-// Fill from one sweep is cleaned by the next sweep at the same block
-// position, so every step touches only two kB x kB blocks (band storage keeps
-// 2kB+1 diagonals per column).  Each step stages the blocks in the warp's
-// shared-memory slice; lanes own rows.
+//   right-apply the previous reflector to the off-diagonal block C = A[R', R],
+//   annihilate C's first column with a new reflector, left-apply it to the
+//   rest of C, two-sided apply it to the diagonal block D = A[R', R'].
+// Fill left by one sweep is cleaned by the next sweep at the same block
+// position, so a step touches only C and D (band storage keeps 2kB+1
+// diagonals per column).
+//
+// A step never reads what the previous step of the same sweep wrote, so the
+// blocks of step k+1 are prefetched while step k computes: C into registers
+// (lane = row), D into a shared-memory double buffer by cp.async.  Warps pull
+// solves from an atomic work counter (persistent kernel).
 #include "common.cuh"
 
 namespace eigenid_b200 {
 
 constexpr int kCB = 32;              // bandwidth (must match band.cu kB)
 constexpr int kCLD = 2 * kCB + 1;    // band diagonals stored per column
-constexpr int kWarpsPerCta = 4;
+constexpr int kWarpsPerCta = 8;
 constexpr int kSLD = kCB + 1;
-constexpr int kWarpSmem = 2 * kCB * kSLD + 4 * kCB;
+constexpr int kBlk = kCB * kSLD;
+constexpr int kWarpSmem = 3 * kBlk + 3 * kCB;  // sC, sD[2], v, v2, w
 
 struct Stage2Args {
   double* band;            // per solve: m columns x kCLD
@@ -32,10 +36,20 @@ struct Stage2Args {
   double* e2;              // per solve: m-1 squared off-diagonal
   double* ae;              // per solve: m-1 |off-diagonal|
   long long de_stride;
+  int* counter;            // work queue (zeroed before launch)
 };
 
-// Householder from x (lane r holds x_r, r < L); returns tau, writes v (v_0=1)
-// to sv, beta to *beta.
+__device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool ok) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr),
+               "l"(gmem), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cpa_commit2() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cpa_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// Householder from x (lane r holds x_r, r < L): v (v_0 = 1) -> sv, returns
+// tau, *beta.  dlarfg convention.
 __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
                                                    double* beta) {
   const int lane = threadIdx.x & 31;
@@ -51,143 +65,177 @@ __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
     tau = (b - alpha) / b;
     scal = 1.0 / (alpha - b);
   }
-  if (lane < kCB) sv[lane] = (lane == 0) ? 1.0 : ((lane < L) ? x * scal : 0.0);
+  sv[lane] = (lane == 0) ? 1.0 : ((lane < L) ? x * scal : 0.0);
   __syncwarp();
   *beta = b;
   return tau;
 }
 
-// D (L x L, full symmetric in sD) <- H D H, H = I - tau v v^T.
-__device__ __forceinline__ void warp_two_sided(double* sD, int L,
-                                               const double* sv, double tau,
-                                               double* sw) {
+// D <- H D H on the L x L diagonal block whose lower triangle sits in sD
+// (filled by cp.async; rows/cols >= L are zero).  Writes the lower triangle
+// back to the band.
+__device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
+                                                double tau, double* sw, int L,
+                                                double* AB, int R) {
   const int lane = threadIdx.x & 31;
+  // mirror lower -> upper
+#pragma unroll 8
+  for (int c = 0; c < kCB; ++c)
+    if (c > lane) sD[lane * kSLD + c] = sD[c * kSLD + lane];
+  __syncwarp();
+  double drow[kCB];
   double p = 0.0;
-  if (lane < L) {
-    const double* row = sD + lane * kSLD;
-    for (int c = 0; c < L; ++c) p += row[c] * sv[c];
-    p *= tau;
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) {
+    drow[c] = sD[lane * kSLD + c];
+    p += drow[c] * sv[c];
   }
-  const double K = 0.5 * tau * warp_sum(lane < L ? p * sv[lane] : 0.0);
-  const double w = p - K * (lane < L ? sv[lane] : 0.0);
+  p *= tau;
+  const double vr = sv[lane];
+  const double K = 0.5 * tau * warp_sum(p * vr);
+  const double w = p - K * vr;
   sw[lane] = w;
   __syncwarp();
-  if (lane < L) {
-    double* row = sD + lane * kSLD;
-    const double vr = sv[lane];
-    for (int c = 0; c < L; ++c) row[c] -= vr * sw[c] + w * sv[c];
-  }
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) drow[c] -= vr * sw[c] + w * sv[c];
+  // lower triangle back to the band: column c, rows c..L-1 (coalesced in r)
+#pragma unroll
+  for (int c = 0; c < kCB; ++c)
+    if (lane >= c && lane < L) AB[(long long)(R + c) * kCLD + (lane - c)] = drow[c];
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
+                                           int L) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 8
+  for (int c = 0; c < kCB; ++c) {
+    const bool ok = lane >= c && lane < L && c < L;
+    cpa8(sD + lane * kSLD + c, ok ? AB + (long long)(R + c) * kCLD + (lane - c) : AB, ok);
+  }
+  cpa_commit2();
+}
+
+__device__ __forceinline__ void load_c(double (&cr)[kCB], const double* AB,
+                                       int R1, int L1, int R, int L) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < kCB; ++c)
+    cr[c] = (lane < L1 && c < L)
+                ? AB[(long long)(R + c) * kCLD + (R1 + lane - R - c)]
+                : 0.0;
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 1)
 bulge_chase_kernel(Stage2Args a) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sidx = blockIdx.x * kWarpsPerCta + warp;
-  if (sidx >= a.nsolves) return;
   double* sC = smem + warp * kWarpSmem;
-  double* sD = sC + kCB * kSLD;
-  double* sv = sD + kCB * kSLD;
+  double* sDb[2] = {sC + kBlk, sC + 2 * kBlk};
+  double* sv = sC + 3 * kBlk;
   double* sv2 = sv + kCB;
   double* sw = sv2 + kCB;
-  const int m = a.js[sidx] < 0 ? a.n : a.n - 1;
-  double* AB = a.band + sidx * a.band_stride;
-  auto at = [&](int r, int c) -> double& {  // r >= c, r - c <= 2kB
-    return AB[(long long)c * kCLD + (r - c)];
-  };
 
-  for (int st = 0; st + 2 < m; ++st) {
-    // ---- block 0: annihilate column st below the subdiagonal
-    int R = st + 1;
-    int L = min(kCB, m - 1 - st);
-    double beta;
-    const double x = lane < L ? at(st + 1 + lane, st) : 0.0;
-    double tau = warp_householder(x, L, sv, &beta);
-    if (lane < L) at(st + 1 + lane, st) = (lane == 0) ? beta : 0.0;
-    // diagonal block D = A[R.., R..]
-    for (int c = 0; c < L; ++c)
-      if (lane >= c && lane < L) {
-        const double v = at(R + lane, R + c);
-        sD[lane * kSLD + c] = v;
-        sD[c * kSLD + lane] = v;
+  for (;;) {
+    int sidx = 0;
+    if (lane == 0) sidx = atomicAdd(a.counter, 1);
+    sidx = __shfl_sync(0xffffffffu, sidx, 0);
+    if (sidx >= a.nsolves) break;
+    const int m = a.js[sidx] < 0 ? a.n : a.n - 1;
+    double* AB = a.band + sidx * a.band_stride;
+
+    for (int st = 0; st + 2 < m; ++st) {
+      __syncwarp();
+      const int R0 = st + 1;
+      const int L0 = min(kCB, m - 1 - st);
+      // block 0 operands; prefetch block 1
+      const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
+      prefetch_d(sDb[0], AB, R0, L0);
+      int Rk = R0 + kCB;
+      bool have = Rk <= m - 1;
+      int Lk = have ? min(kCB, m - Rk) : 0;
+      double ncrow[kCB];
+      if (have) {
+        load_c(ncrow, AB, Rk, Lk, R0, L0);
+        prefetch_d(sDb[1], AB, Rk, Lk);
       }
-    __syncwarp();
-    warp_two_sided(sD, L, sv, tau, sw);
-    for (int c = 0; c < L; ++c)
-      if (lane >= c && lane < L) at(R + lane, R + c) = sD[lane * kSLD + c];
-    __syncwarp();
-    // ---- chase
-    while (true) {
-      const int R1 = R + kCB;
-      if (R1 > m - 1) break;
-      const int L1 = min(kCB, m - R1);
-      // C = A[R1.., R..] (L1 x L); lane = row
-      double crow[kCB];
+      double beta;
+      double tau = warp_householder(x, L0, sv, &beta);
+      if (lane < L0) AB[(long long)st * kCLD + 1 + lane] = (lane == 0) ? beta : 0.0;
+      if (have) cpa_wait_one(); else cpa_wait_all();
+      __syncwarp();
+      two_sided_store(sDb[0], sv, tau, sw, L0, AB, R0);
+      int R = R0, L = L0, buf = 1;
+      while (have) {
+        // ---- step on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]
+        double crow[kCB];
 #pragma unroll
-      for (int c = 0; c < kCB; ++c)
-        crow[c] = (lane < L1 && c < L) ? at(R1 + lane, R + c) : 0.0;
-      // right apply previous H: C -= tau (C v) v^T
-      double y = 0.0;
+        for (int c = 0; c < kCB; ++c) crow[c] = ncrow[c];
+        const int Rn = Rk + kCB;
+        const bool haven = Rn <= m - 1;
+        const int Ln = haven ? min(kCB, m - Rn) : 0;
+        __syncwarp();
+        if (haven) {
+          load_c(ncrow, AB, Rn, Ln, Rk, Lk);
+          prefetch_d(sDb[buf ^ 1], AB, Rn, Ln);
+        }
+        // right-apply the previous reflector: C -= tau (C v) v^T
+        double y = 0.0;
 #pragma unroll
-      for (int c = 0; c < kCB; ++c) y += crow[c] * sv[c];
-      y *= tau;
+        for (int c = 0; c < kCB; ++c) y += crow[c] * sv[c];
+        y *= tau;
 #pragma unroll
-      for (int c = 0; c < kCB; ++c) crow[c] -= y * sv[c];
-      // new reflector from column 0
-      double beta2;
-      const double tau2 = warp_householder(crow[0], L1, sv2, &beta2);
-      crow[0] = (lane == 0) ? beta2 : 0.0;
-      // left apply to columns 1..: w_c = sum_r v2_r C[r][c]
-      if (lane < kCB) {
+        for (int c = 0; c < kCB; ++c) crow[c] -= y * sv[c];
+        // new reflector from C's first column
+        double beta2;
+        const double tau2 = warp_householder(crow[0], Lk, sv2, &beta2);
+        crow[0] = (lane == 0) ? beta2 : 0.0;
+        // left-apply to columns 1..L-1: w_c = sum_r v2_r C[r][c]
 #pragma unroll
         for (int c = 0; c < kCB; ++c) sC[lane * kSLD + c] = crow[c];
-      }
-      __syncwarp();
-      {
-        double w = 0.0;
-        if (lane >= 1 && lane < L)
-          for (int r = 0; r < L1; ++r) w += sv2[r] * sC[r * kSLD + lane];
-        sw[lane] = tau2 * w;
-      }
-      __syncwarp();
-      if (lane < L1) {
-        const double vr = sv2[lane];
-#pragma unroll
-        for (int c = 1; c < kCB; ++c) crow[c] -= vr * sw[c];
-      }
-#pragma unroll
-      for (int c = 0; c < kCB; ++c)
-        if (lane < L1 && c < L) at(R1 + lane, R + c) = crow[c];
-      __syncwarp();
-      // two-sided on the next diagonal block
-      for (int c = 0; c < L1; ++c)
-        if (lane >= c && lane < L1) {
-          const double v = at(R1 + lane, R1 + c);
-          sD[lane * kSLD + c] = v;
-          sD[c * kSLD + lane] = v;
+        __syncwarp();
+        {
+          double w = 0.0;
+#pragma unroll 8
+          for (int r = 0; r < kCB; ++r) w += sv2[r] * sC[r * kSLD + lane];
+          sw[lane] = (lane >= 1 && lane < L) ? tau2 * w : 0.0;
         }
-      __syncwarp();
-      warp_two_sided(sD, L1, sv2, tau2, sw);
-      for (int c = 0; c < L1; ++c)
-        if (lane >= c && lane < L1) at(R1 + lane, R1 + c) = sD[lane * kSLD + c];
-      __syncwarp();
-      if (lane < kCB) sv[lane] = sv2[lane];
-      __syncwarp();
-      tau = tau2;
-      R = R1;
-      L = L1;
+        __syncwarp();
+        {
+          const double vr = sv2[lane];
+#pragma unroll
+          for (int c = 1; c < kCB; ++c) crow[c] -= vr * sw[c];
+        }
+#pragma unroll
+        for (int c = 0; c < kCB; ++c)
+          if (lane < Lk && c < L)
+            AB[(long long)(R + c) * kCLD + (Rk + lane - R - c)] = crow[c];
+        // two-sided on the diagonal block (prefetched into sDb[buf])
+        if (haven) cpa_wait_one(); else cpa_wait_all();
+        __syncwarp();
+        two_sided_store(sDb[buf], sv2, tau2, sw, Lk, AB, Rk);
+        sv[lane] = sv2[lane];
+        __syncwarp();
+        tau = tau2;
+        R = Rk;
+        L = Lk;
+        Rk = Rn;
+        Lk = Ln;
+        have = haven;
+        buf ^= 1;
+      }
     }
-  }
-  double* d = a.d + sidx * a.de_stride;
-  double* e2 = a.e2 + sidx * a.de_stride;
-  double* ae = a.ae + sidx * a.de_stride;
-  for (int k = lane; k < m; k += 32) {
-    d[k] = at(k, k);
-    if (k + 1 < m) {
-      const double e = at(k + 1, k);
-      e2[k] = e * e;
-      ae[k] = fabs(e);
+    __syncwarp();
+    double* d = a.d + sidx * a.de_stride;
+    double* e2 = a.e2 + sidx * a.de_stride;
+    double* ae = a.ae + sidx * a.de_stride;
+    for (int k = lane; k < m; k += 32) {
+      d[k] = AB[(long long)k * kCLD];
+      if (k + 1 < m) {
+        const double e = AB[(long long)k * kCLD + 1];
+        e2[k] = e * e;
+        ae[k] = fabs(e);
+      }
     }
   }
 }
@@ -197,7 +245,12 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(
       bulge_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = (a.nsolves + kWarpsPerCta - 1) / kWarpsPerCta;
+  e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int need = (a.nsolves + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int grid = need < sms ? need : sms;
   bulge_chase_kernel<<<grid, kWarpsPerCta * 32, smem, st>>>(a);
   return cudaGetLastError();
 }

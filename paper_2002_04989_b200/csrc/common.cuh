@@ -54,37 +54,67 @@ __device__ __forceinline__ void set_status(DevStatus* st, int code,
 }
 
 // Sturm count: number of eigenvalues of the symmetric tridiagonal (d, e2)
-// strictly below x (LAPACK dlaebz convention: a zero pivot is replaced by
-// -pivmin and counts as negative).  e2[k] = offdiag[k]^2, k = 0..m-2.
+// strictly below x, division-free form p_k = (d_k - x) p_{k-1} - e2_{k-1}
+// p_{k-2}, counting sign changes (Sturm sequence of leading minors).  The
+// caller pre-scales (d, e2, x) by an exact power of two so that ||T|| <= 1,
+// which bounds growth per step by 3; both p's are renormalised by a power of
+// two every 4 steps.  A zero p_k is replaced by -p_{k-1} 2^-900, the p-form
+// image of LAPACK dlaebz's q = -pivmin convention.  3 DP ops per step versus
+// ~20 for the division of the q-form.
 __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
                                            const double* __restrict__ e2,
-                                           int m, double x, double pivmin) {
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  int cnt = q < 0.0;
-  for (int k = 1; k < m; ++k) {
-    q = (d[k] - x) - e2[k - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
+                                           int m, double x) {
+  double p0 = 1.0, p1 = d[0] - x;
+  if (p1 == 0.0) p1 = -0x1p-900;
+  int cnt = __double2hiint(p1) < 0;
+  int k = 1;
+  for (; k + 4 <= m; k += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double p2 = fma(d[k + u] - x, p1, -e2[k + u - 1] * p0);
+      if (p2 == 0.0) p2 = -p1 * 0x1p-900;
+      cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+      p0 = p1;
+      p1 = p2;
+    }
+    const double mx = fmax(fabs(p0), fabs(p1));
+    if (mx > 0x1p256 || mx < 0x1p-256) {
+      const double f = scalbn(1.0, -ilogb(mx));
+      p0 *= f;
+      p1 *= f;
+    }
+  }
+  for (; k < m; ++k) {
+    double p2 = fma(d[k] - x, p1, -e2[k - 1] * p0);
+    if (p2 == 0.0) p2 = -p1 * 0x1p-900;
+    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+    p0 = p1;
+    p1 = p2;
   }
   return cnt;
 }
 
-// Bisects eigenvalue k (0-based, ascending) of (d, e2) inside [lo, hi) with
-// count(lo) <= k < count(hi) already established.  Stops at
+// Power-of-two scale 2^-e with 2^e >= tn (exact rescaling of T).
+__device__ __forceinline__ double pow2_scale(double tn) {
+  if (!(tn > 0.0)) return 1.0;
+  return scalbn(1.0, -(ilogb(tn) + 1));
+}
+
+// Bisects eigenvalue k (0-based, ascending) of the scaled (d, e2) inside
+// [lo, hi) with count(lo) <= k < count(hi) already established.  Stops at
 // hi - lo <= max(atol, 2 eps max(|lo|,|hi|)) — the accuracy the
 // Householder reduction's backward error (~eps ||T||) supports.
 __device__ __forceinline__ double bisect_one(const double* __restrict__ d,
                                              const double* __restrict__ e2,
                                              int m, int k, double lo, double hi,
-                                             double atol, double pivmin) {
+                                             double atol) {
   for (int it = 0; it < 200; ++it) {
     const double w = hi - lo;
     const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
     if (w <= tol) break;
     const double mid = lo + 0.5 * w;
     if (mid <= lo || mid >= hi) break;
-    if (sturm_count(d, e2, m, mid, pivmin) > k)
+    if (sturm_count(d, e2, m, mid) > k)
       hi = mid;
     else
       lo = mid;

@@ -91,28 +91,33 @@ __device__ void warp_tridiagonalize(double* S, int ld, int m, double* d,
 
 // All eigenvalues of (d, e2) by lane-per-eigenvalue bisection from the
 // Gershgorin interval; writes ascending values to out[0..m).
-__device__ void warp_bisect_all(const double* d, const double* e2,
-                                const double* ae, int m, double* out) {
+__device__ void warp_bisect_all(double* d, double* e2, const double* ae, int m,
+                                double* out) {
   const int lane = threadIdx.x & 31;
-  double lo = 1e308, hi = -1e308, tn = 0.0, emax = 0.0;
+  double lo = 1e308, hi = -1e308, tn = 0.0;
   for (int k = lane; k < m; k += 32) {
     const double r = (k > 0 ? ae[k - 1] : 0.0) + (k + 1 < m ? ae[k] : 0.0);
     lo = fmin(lo, d[k] - r);
     hi = fmax(hi, d[k] + r);
     tn = fmax(tn, fabs(d[k]) + r);
-    if (k + 1 < m) emax = fmax(emax, e2[k]);
   }
   lo = warp_min(lo);
   hi = warp_max(hi);
   tn = warp_max(tn);
-  emax = warp_max(emax);
-  const double pivmin = kSafeMin * fmax(1.0, emax);
-  const double fudge = 2.0 * kEps * tn * m + 2.0 * pivmin;
-  lo -= fudge;
-  hi += fudge;
-  const double atol = kEps * tn;
+  // exact power-of-two scaling to ||T|| <= 1 for the division-free count
+  const double sc = pow2_scale(tn);
+  __syncwarp();
+  for (int k = lane; k < m; k += 32) {
+    d[k] *= sc;
+    if (k + 1 < m) e2[k] *= sc * sc;
+  }
+  __syncwarp();
+  const double fudge = 2.0 * kEps * tn * m + 1e-300;
+  lo = (lo - fudge) * sc;
+  hi = (hi + fudge) * sc;
+  const double atol = kEps * tn * sc;
   for (int k = lane; k < m; k += 32)
-    out[k] = bisect_one(d, e2, m, k, lo, hi, atol, pivmin);
+    out[k] = bisect_one(d, e2, m, k, lo, hi, atol) / sc;
   __syncwarp();
   // Bisection results are monotone up to the stopping tolerance; enforce the
   // ascending contract of Spectrum (eigensolve.hpp:10-11) exactly.
