@@ -626,10 +626,11 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
       for (int nt = 0; nt < 4; ++nt) {
         const int col = cb + 32 * wn + 8 * nt + 2 * kk;
         if (r < s && col + 1 < s) {
-          const double2 x =
-              *reinterpret_cast<const double2*>(A22 + (long long)r * ldw + col);
-          c[mt][nt][0] = x.x;
-          c[mt][nt][1] = x.y;
+          // volatile: keeps the prefetch ahead of the (volatile) DMMAs of the
+          // current tile instead of letting the scheduler sink it to its use
+          asm volatile("ld.global.v2.f64 {%0, %1}, [%2];\n"
+                       : "=d"(c[mt][nt][0]), "=d"(c[mt][nt][1])
+                       : "l"(A22 + (long long)r * ldw + col));
         } else {
           c[mt][nt][0] = (r < s && col < s) ? A22[(long long)r * ldw + col] : 0.0;
           c[mt][nt][1] = 0.0;
@@ -725,7 +726,28 @@ __device__ void write_band(const double* W, int ldw, int m, int c_begin,
   }
 }
 
+#ifdef EIGENID_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+#define PHASE(id)                                                         \
+  do {                                                                    \
+    __syncthreads();                                                      \
+    const long long now_ = clock64();                                     \
+    if (threadIdx.x == 0 && blockIdx.x == 0)                              \
+      atomicAdd(&g_phase_cycles[ph_], (unsigned long long)(now_ - t_ph_)); \
+    t_ph_ = now_;                                                         \
+    ph_ = (id);                                                           \
+  } while (0)
+#else
+#define PHASE(id) \
+  do {            \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
+#ifdef EIGENID_PHASE_TIMING
+  long long t_ph_ = clock64();
+  int ph_ = 0;
+#endif
   extern __shared__ double smem[];
   double* sgemm = smem;
   double* sT = smem + kGemmSmem;
@@ -750,20 +772,21 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
     const int j = args.js[sidx];
     const int m = j < 0 ? n : n - 1;
     double* band = args.band + sidx * args.band_stride;
+    PHASE(1);
     // materialise the lower triangle of the minor (r' = r + (r >= j))
     for (int r = warp; r < m; r += kNT / 32) {
       const int rr = (j >= 0 && r >= j) ? r + 1 : r;
       const double* src = args.A + (long long)rr * n;
       double* dst = W + (long long)r * ldw;
-      for (int c0 = lane; c0 <= r; c0 += 128) {
-        double v[4];
+      for (int c0 = lane; c0 <= r; c0 += 512) {
+        double v[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 16; ++u) {
           const int cc = c0 + 32 * u;
           v[u] = cc <= r ? src[(j >= 0 && cc >= j) ? cc + 1 : cc] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 16; ++u)
           if (c0 + 32 * u <= r) dst[c0 + 32 * u] = v[u];
       }
     }
@@ -774,6 +797,7 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
       if (s < 2) break;
       const int c0 = c + kB;
       double* P0 = W + (long long)c0 * ldw + c;
+      PHASE(2);
       const bool fast = s >= 2 * kB &&
                         chol_panel(P0, ldw, s, Vg, Xg, sT, sG, sA, sB, sR, sS,
                                    sgemm, sflag);
@@ -796,10 +820,13 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
         }
       }
       __syncthreads();
+      PHASE(3);
       write_band(W, ldw, m, c, c + kB, band);
       row_transform(Vg, kB, sT, 1.0, nullptr, VTg, s);       // VT = V T
       double* A22 = W + (long long)c0 * ldw + c0;
+      PHASE(4);
       gemm1(A22, ldw, s, VTg, Xg, sgemm);                     // X = A22 VT
+      PHASE(5);
       gram(Vg, kB, Xg, kB, s, sG, sgemm);                     // Y = V^T X
       for (int t = tid; t < kB * kB; t += kNT) {              // M = T^T Y
         const int q = t / kB, p = t % kB;
@@ -809,12 +836,21 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
       }
       __syncthreads();
       row_transform(Vg, kB, sM, -0.5, Xg, Xg, s);             // W2 = X - V M/2
+      PHASE(6);
       gemm2(A22, ldw, s, Xg, Vg, sgemm);                      // A22 -= W2V^T+VW2^T
+      PHASE(7);
     }
     write_band(W, ldw, m, c, m, band);
     __syncthreads();
   }
+  PHASE(0);
 }
+
+#ifdef EIGENID_PHASE_TIMING
+extern "C" void eigenid_debug_phase_cycles(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+}
+#endif
 
 size_t stage1_smem_bytes() { return sizeof(double) * (size_t)kStage1SmemDoubles; }
 int stage1_band_ld() { return kLDAB; }

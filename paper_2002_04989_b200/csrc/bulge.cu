@@ -11,10 +11,16 @@
 // position, so a step touches only C and D (band storage keeps 2kB+1
 // diagonals per column).
 //
-// A step never reads what the previous step of the same sweep wrote, so the
-// blocks of step k+1 are prefetched while step k computes: C into registers
-// (lane = row), D into a shared-memory double buffer by cp.async.  Warps pull
-// solves from an atomic work counter (persistent kernel).
+// A CTA owns one solve at a time and its 8 warps chase 8 consecutive sweeps
+// concurrently (warp w takes sweeps w, w+8, ...): sweep s may run step k once
+// sweep s-1 has finished step k+1 (k+2 before prefetching step k+1), tracked
+// by per-warp progress counters in shared memory.  The leading sweep pulls
+// each block from HBM and the 7 following sweeps re-read it from L2/L1, so
+// band traffic to HBM drops ~8x versus independent solves per warp.  Within
+// a sweep a step never reads what the previous step wrote, so the blocks of
+// step k+1 are prefetched while step k computes (C into registers, lane =
+// row; the full symmetric D into a shared-memory double buffer by cp.async).
+// CTAs pull solves from an atomic work counter (persistent kernel).
 #include "common.cuh"
 
 namespace eigenid_b200 {
@@ -71,25 +77,21 @@ __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
   return tau;
 }
 
-// D <- H D H on the L x L diagonal block whose lower triangle sits in sD
+// D <- H D H on the L x L diagonal block held (both triangles) in sD
 // (filled by cp.async; rows/cols >= L are zero).  Writes the lower triangle
 // back to the band.
 __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
                                                 double tau, double* sw, int L,
                                                 double* AB, int R) {
   const int lane = threadIdx.x & 31;
-  // mirror lower -> upper
-#pragma unroll 8
-  for (int c = 0; c < kCB; ++c)
-    if (c > lane) sD[lane * kSLD + c] = sD[c * kSLD + lane];
-  __syncwarp();
   double drow[kCB];
-  double p = 0.0;
+  double pp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < kCB; ++c) {
     drow[c] = sD[lane * kSLD + c];
-    p += drow[c] * sv[c];
+    pp[c & 3] += drow[c] * sv[c];
   }
+  double p = (pp[0] + pp[1]) + (pp[2] + pp[3]);
   p *= tau;
   const double vr = sv[lane];
   const double K = 0.5 * tau * warp_sum(p * vr);
@@ -107,11 +109,14 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
 
 __device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
                                            int L) {
+  // full symmetric L x L block: element (r, c) lives at column min(r,c),
+  // diagonal |r - c| of the band; out-of-range entries are zero-filled
   const int lane = threadIdx.x & 31;
 #pragma unroll 8
   for (int c = 0; c < kCB; ++c) {
-    const bool ok = lane >= c && lane < L && c < L;
-    cpa8(sD + lane * kSLD + c, ok ? AB + (long long)(R + c) * kCLD + (lane - c) : AB, ok);
+    const bool ok = lane < L && c < L;
+    const int lo = min(lane, c), df = abs(lane - c);
+    cpa8(sD + lane * kSLD + c, ok ? AB + (long long)(R + lo) * kCLD + df : AB, ok);
   }
   cpa_commit2();
 }
@@ -126,9 +131,52 @@ __device__ __forceinline__ void load_c(double (&cr)[kCB], const double* AB,
                 : 0.0;
 }
 
+#ifdef EIGENID_PHASE_TIMING
+__device__ unsigned long long g_bulge_cycles[8];
+#define BPH(id)                                                         \
+  do {                                                                  \
+    const long long now_ = clock64();                                   \
+    if (lane == 0 && blockIdx.x == 0 && warp == 0)                      \
+      g_bulge_cycles[id] += (unsigned long long)(now_ - t_b_);          \
+    t_b_ = now_;                                                        \
+  } while (0)
+#else
+#define BPH(id) \
+  do {          \
+  } while (0)
+#endif
+
+__device__ __forceinline__ long long spos(int sweep, int step) {
+  return (long long)sweep * 65536 + step;
+}
+
+// Blocks until sweep s-1 (owned by warp (w-1) mod 8) has finished step k.
+__device__ __forceinline__ void wait_prev(volatile long long* prog, int warp,
+                                          int s, int k) {
+  if (s == 0) return;
+  const int pw = (warp + kWarpsPerCta - 1) % kWarpsPerCta;
+  const long long need = spos(s - 1, k);
+  if ((threadIdx.x & 31) == 0)
+    while (prog[pw] < need) __nanosleep(64);
+  __syncwarp();
+  __threadfence_block();
+}
+
+__device__ __forceinline__ void publish(volatile long long* prog, int warp,
+                                        int s, int k) {
+  __syncwarp();
+  __threadfence_block();
+  if ((threadIdx.x & 31) == 0) prog[warp] = spos(s, k);
+}
+
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 1)
 bulge_chase_kernel(Stage2Args a) {
+#ifdef EIGENID_PHASE_TIMING
+  long long t_b_ = clock64();
+#endif
   extern __shared__ double smem[];
+  __shared__ long long prog[kWarpsPerCta];
+  __shared__ int s_sidx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sC = smem + warp * kWarpSmem;
   double* sDb[2] = {sC + kBlk, sC + 2 * kBlk};
@@ -137,23 +185,25 @@ bulge_chase_kernel(Stage2Args a) {
   double* sw = sv2 + kCB;
 
   for (;;) {
-    int sidx = 0;
-    if (lane == 0) sidx = atomicAdd(a.counter, 1);
-    sidx = __shfl_sync(0xffffffffu, sidx, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) s_sidx = atomicAdd(a.counter, 1);
+    if (threadIdx.x < kWarpsPerCta) prog[threadIdx.x] = -1;
+    __syncthreads();
+    const int sidx = s_sidx;
     if (sidx >= a.nsolves) break;
     const int m = a.js[sidx] < 0 ? a.n : a.n - 1;
     double* AB = a.band + sidx * a.band_stride;
 
-    for (int st = 0; st + 2 < m; ++st) {
-      __syncwarp();
+    for (int st = warp; st + 2 < m; st += kWarpsPerCta) {
       const int R0 = st + 1;
       const int L0 = min(kCB, m - 1 - st);
-      // block 0 operands; prefetch block 1
-      const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
-      prefetch_d(sDb[0], AB, R0, L0);
       int Rk = R0 + kCB;
       bool have = Rk <= m - 1;
       int Lk = have ? min(kCB, m - Rk) : 0;
+      // block 0 and the prefetch of step 1 need sweep st-1 past step 2
+      wait_prev(prog, warp, st, 2);
+      const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
+      prefetch_d(sDb[0], AB, R0, L0);
       double ncrow[kCB];
       if (have) {
         load_c(ncrow, AB, Rk, Lk, R0, L0);
@@ -165,39 +215,44 @@ bulge_chase_kernel(Stage2Args a) {
       if (have) cpa_wait_one(); else cpa_wait_all();
       __syncwarp();
       two_sided_store(sDb[0], sv, tau, sw, L0, AB, R0);
-      int R = R0, L = L0, buf = 1;
+      publish(prog, warp, st, 0);
+      int R = R0, L = L0, buf = 1, k = 1;
       while (have) {
-        // ---- step on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]
+        // ---- step k on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]
         double crow[kCB];
 #pragma unroll
         for (int c = 0; c < kCB; ++c) crow[c] = ncrow[c];
         const int Rn = Rk + kCB;
         const bool haven = Rn <= m - 1;
         const int Ln = haven ? min(kCB, m - Rn) : 0;
-        __syncwarp();
+        BPH(0);
         if (haven) {
+          wait_prev(prog, warp, st, k + 2);
           load_c(ncrow, AB, Rn, Ln, Rk, Lk);
           prefetch_d(sDb[buf ^ 1], AB, Rn, Ln);
         }
+        BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
-        double y = 0.0;
+        double yy[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int c = 0; c < kCB; ++c) y += crow[c] * sv[c];
-        y *= tau;
+        for (int c = 0; c < kCB; ++c) yy[c & 3] += crow[c] * sv[c];
+        const double y = tau * ((yy[0] + yy[1]) + (yy[2] + yy[3]));
 #pragma unroll
         for (int c = 0; c < kCB; ++c) crow[c] -= y * sv[c];
         // new reflector from C's first column
         double beta2;
         const double tau2 = warp_householder(crow[0], Lk, sv2, &beta2);
         crow[0] = (lane == 0) ? beta2 : 0.0;
+        BPH(2);
         // left-apply to columns 1..L-1: w_c = sum_r v2_r C[r][c]
 #pragma unroll
         for (int c = 0; c < kCB; ++c) sC[lane * kSLD + c] = crow[c];
         __syncwarp();
         {
-          double w = 0.0;
-#pragma unroll 8
-          for (int r = 0; r < kCB; ++r) w += sv2[r] * sC[r * kSLD + lane];
+          double ww[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int r = 0; r < kCB; ++r) ww[r & 3] += sv2[r] * sC[r * kSLD + lane];
+          const double w = (ww[0] + ww[1]) + (ww[2] + ww[3]);
           sw[lane] = (lane >= 1 && lane < L) ? tau2 * w : 0.0;
         }
         __syncwarp();
@@ -210,12 +265,15 @@ bulge_chase_kernel(Stage2Args a) {
         for (int c = 0; c < kCB; ++c)
           if (lane < Lk && c < L)
             AB[(long long)(R + c) * kCLD + (Rk + lane - R - c)] = crow[c];
+        BPH(3);
         // two-sided on the diagonal block (prefetched into sDb[buf])
         if (haven) cpa_wait_one(); else cpa_wait_all();
         __syncwarp();
+        BPH(4);
         two_sided_store(sDb[buf], sv2, tau2, sw, Lk, AB, Rk);
+        BPH(5);
         sv[lane] = sv2[lane];
-        __syncwarp();
+        publish(prog, warp, st, k);
         tau = tau2;
         R = Rk;
         L = Lk;
@@ -223,13 +281,15 @@ bulge_chase_kernel(Stage2Args a) {
         Lk = Ln;
         have = haven;
         buf ^= 1;
+        ++k;
       }
+      publish(prog, warp, st, 65535);  // sweep done
     }
-    __syncwarp();
+    __syncthreads();
     double* d = a.d + sidx * a.de_stride;
     double* e2 = a.e2 + sidx * a.de_stride;
     double* ae = a.ae + sidx * a.de_stride;
-    for (int k = lane; k < m; k += 32) {
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
       d[k] = AB[(long long)k * kCLD];
       if (k + 1 < m) {
         const double e = AB[(long long)k * kCLD + 1];
@@ -240,6 +300,12 @@ bulge_chase_kernel(Stage2Args a) {
   }
 }
 
+#ifdef EIGENID_PHASE_TIMING
+extern "C" void eigenid_debug_bulge_cycles(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_bulge_cycles, sizeof(g_bulge_cycles));
+}
+#endif
+
 cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   const size_t smem = sizeof(double) * kWarpSmem * kWarpsPerCta;
   cudaError_t e = cudaFuncSetAttribute(
@@ -249,8 +315,7 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int need = (a.nsolves + kWarpsPerCta - 1) / kWarpsPerCta;
-  const int grid = need < sms ? need : sms;
+  const int grid = a.nsolves < sms ? a.nsolves : sms;
   bulge_chase_kernel<<<grid, kWarpsPerCta * 32, smem, st>>>(a);
   return cudaGetLastError();
 }

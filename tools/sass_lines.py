@@ -46,3 +46,27 @@ for (f, l), v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
             files[f] = []
     txt = files[f][l - 1].strip()[:72] if l and len(files[f]) >= l else ''
     print(f'{100 * v / tot:5.1f}% {f}:{l}  {txt}')
+
+# per-reason breakdown of the top lines
+reasons = [c for c in h if c.startswith('stall_') and '(Not Issued)' not in c]
+ri = [h.index(c) for c in reasons]
+per = {}
+for r in rows[2:]:
+    try:
+        a = int(r[0], 16)
+    except (ValueError, IndexError):
+        continue
+    ln = off2line.get(a - base, ('?', 0))
+    vals = per.setdefault(ln, [0.0] * len(ri))
+    for t, i in enumerate(ri):
+        try:
+            vals[t] += float(r[i])
+        except ValueError:
+            pass
+tot_r = [sum(v[t] for v in per.values()) for t in range(len(ri))]
+print('overall:', ', '.join(f'{reasons[t][6:]}={100*tot_r[t]/max(sum(tot_r),1):.1f}%'
+                           for t in sorted(range(len(ri)), key=lambda t: -tot_r[t])[:8]))
+for (f, l), v in sorted(per.items(), key=lambda x: -sum(x[1]))[:12]:
+    s = sum(v)
+    top = sorted(range(len(ri)), key=lambda t: -v[t])[:3]
+    print(f'{f}:{l}', ', '.join(f'{reasons[t][6:]}={100*v[t]/max(s,1):.0f}%' for t in top))
