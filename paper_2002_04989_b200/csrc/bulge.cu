@@ -50,6 +50,15 @@ __device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool ok) 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr),
                "l"(gmem), "r"(ok ? 8 : 0));
 }
+// Branch-free predicated store (the compiler otherwise emits one divergent
+// branch per element of the 32-iteration store loops).
+__device__ __forceinline__ void st_pred(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}\n" ::"l"(p),
+      "d"(v), "r"((int)pred)
+      : "memory");
+}
+
 __device__ __forceinline__ void cpa_commit2() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cpa_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
@@ -101,9 +110,10 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
 #pragma unroll
   for (int c = 0; c < kCB; ++c) drow[c] -= vr * sw[c] + w * sv[c];
   // lower triangle back to the band: column c, rows c..L-1 (coalesced in r)
+  double* base = AB + (long long)R * kCLD + lane;
 #pragma unroll
   for (int c = 0; c < kCB; ++c)
-    if (lane >= c && lane < L) AB[(long long)(R + c) * kCLD + (lane - c)] = drow[c];
+    st_pred(base + c * (kCLD - 1), drow[c], lane >= c && lane < L);
   __syncwarp();
 }
 
@@ -112,11 +122,13 @@ __device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
   // full symmetric L x L block: element (r, c) lives at column min(r,c),
   // diagonal |r - c| of the band; out-of-range entries are zero-filled
   const int lane = threadIdx.x & 31;
-#pragma unroll 8
+  const double* base = AB + (long long)R * kCLD;
+#pragma unroll
   for (int c = 0; c < kCB; ++c) {
     const bool ok = lane < L && c < L;
-    const int lo = min(lane, c), df = abs(lane - c);
-    cpa8(sD + lane * kSLD + c, ok ? AB + (long long)(R + lo) * kCLD + df : AB, ok);
+    // (r, c) -> column min(r,c), diagonal |r-c|
+    const int off = (c <= lane) ? c * kCLD + (lane - c) : lane * kCLD + (c - lane);
+    cpa8(sD + lane * kSLD + c, ok ? base + off : AB, ok);
   }
   cpa_commit2();
 }
@@ -124,11 +136,10 @@ __device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
 __device__ __forceinline__ void load_c(double (&cr)[kCB], const double* AB,
                                        int R1, int L1, int R, int L) {
   const int lane = threadIdx.x & 31;
+  const double* base = AB + (long long)R * kCLD + (R1 - R) + lane;
 #pragma unroll
   for (int c = 0; c < kCB; ++c)
-    cr[c] = (lane < L1 && c < L)
-                ? AB[(long long)(R + c) * kCLD + (R1 + lane - R - c)]
-                : 0.0;
+    cr[c] = (lane < L1 && c < L) ? base[c * (kCLD - 1)] : 0.0;
 }
 
 #ifdef EIGENID_PHASE_TIMING
@@ -261,10 +272,12 @@ bulge_chase_kernel(Stage2Args a) {
 #pragma unroll
           for (int c = 1; c < kCB; ++c) crow[c] -= vr * sw[c];
         }
+        {
+          double* base = AB + (long long)R * kCLD + (Rk - R) + lane;
 #pragma unroll
-        for (int c = 0; c < kCB; ++c)
-          if (lane < Lk && c < L)
-            AB[(long long)(R + c) * kCLD + (Rk + lane - R - c)] = crow[c];
+          for (int c = 0; c < kCB; ++c)
+            st_pred(base + c * (kCLD - 1), crow[c], lane < Lk && c < L);
+        }
         BPH(3);
         // two-sided on the diagonal block (prefetched into sDb[buf])
         if (haven) cpa_wait_one(); else cpa_wait_all();
