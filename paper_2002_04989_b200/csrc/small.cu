@@ -135,51 +135,14 @@ __device__ void warp_bisect_all(double* d, double* e2, const double* ae, int m,
   __syncwarp();
 }
 
-__global__ void small_all_magnitudes_kernel(const double* __restrict__ A,
-                                            int n, int batch, double tol,
-                                            int log_domain,
-                                            double* __restrict__ out,
-                                            double* __restrict__ lambda_out,
-                                            double* __restrict__ mu_out,
-                                            DevStatus* status) {
-  extern __shared__ double sm[];
-  const int nw = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long mat = blockIdx.x;
-  const int ldA = n | 1;  // odd leading dimension: conflict-free columns
-  double* sA = sm;                       // n x ldA
-  double* lam = sA + n * ldA;            // n
-  double* mu = lam + n;                  // n x (n-1)
-  double* wbase = mu + n * (n - 1);      // per-warp scratch
-  const int wsz = n * ldA + 5 * n;
-  double* S = wbase + warp * wsz;
-  double* d = S + n * ldA;
-  double* e2 = d + n;
-  double* ae = e2 + n;
-  double* uu = ae + n;
-  double* qq = uu + n;
-
-  const double* Ag = A + mat * (long long)n * n;
-  for (int t = threadIdx.x; t < n * n; t += blockDim.x)
-    sA[(t / n) * ldA + (t % n)] = Ag[t];
-  __syncthreads();
-
-  // n + 1 solves: s < n is minor M_s, s == n is A itself.
-  for (int s = warp; s <= n; s += nw) {
-    const int m = (s == n) ? n : n - 1;
-    for (int t = lane; t < m * m; t += 32) {
-      const int r = t / m, c = t % m;
-      const int rr = (s < n && r >= s) ? r + 1 : r;
-      const int cc = (s < n && c >= s) ? c + 1 : c;
-      S[r * ldA + c] = sA[rr * ldA + cc];
-    }
-    __syncwarp();
-    warp_tridiagonalize(S, ldA, m, d, e2, ae, uu, qq);
-    warp_bisect_all(d, e2, ae, m, s == n ? lam : mu + s * (n - 1));
-  }
-  __syncthreads();
-
-  // check_fully_nondegenerate (identity.cpp:141-149)
+// Degeneracy check (identity.cpp:141-149) and the identity stage for one
+// matrix whose lambda / mu sit in shared memory (all threads of the CTA).
+__device__ void small_identity_phase(const double* lam, const double* mu, int n,
+                                     int batch, double tol, int log_domain,
+                                     long long mat, double* __restrict__ out,
+                                     double* __restrict__ lambda_out,
+                                     double* __restrict__ mu_out,
+                                     DevStatus* status) {
   __shared__ int degenerate;
   if (threadIdx.x == 0) {
     degenerate = 0;
@@ -226,6 +189,105 @@ __global__ void small_all_magnitudes_kernel(const double* __restrict__ A,
   }
 }
 
+
+__global__ void small_all_magnitudes_kernel(const double* __restrict__ A,
+                                            int n, int batch, double tol,
+                                            int log_domain,
+                                            double* __restrict__ out,
+                                            double* __restrict__ lambda_out,
+                                            double* __restrict__ mu_out,
+                                            DevStatus* status) {
+  extern __shared__ double sm[];
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long mat = blockIdx.x;
+  const int ldA = n | 1;  // odd leading dimension: conflict-free columns
+  double* sA = sm;                       // n x ldA
+  double* lam = sA + n * ldA;            // n
+  double* mu = lam + n;                  // n x (n-1)
+  double* wbase = mu + n * (n - 1);      // per-warp scratch
+  const int wsz = n * ldA + 5 * n;
+  double* S = wbase + warp * wsz;
+  double* d = S + n * ldA;
+  double* e2 = d + n;
+  double* ae = e2 + n;
+  double* uu = ae + n;
+  double* qq = uu + n;
+
+  const double* Ag = A + mat * (long long)n * n;
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x)
+    sA[(t / n) * ldA + (t % n)] = Ag[t];
+  __syncthreads();
+
+  // n + 1 solves: s < n is minor M_s, s == n is A itself.
+  for (int s = warp; s <= n; s += nw) {
+    const int m = (s == n) ? n : n - 1;
+    for (int t = lane; t < m * m; t += 32) {
+      const int r = t / m, c = t % m;
+      const int rr = (s < n && r >= s) ? r + 1 : r;
+      const int cc = (s < n && c >= s) ? c + 1 : c;
+      S[r * ldA + c] = sA[rr * ldA + cc];
+    }
+    __syncwarp();
+    warp_tridiagonalize(S, ldA, m, d, e2, ae, uu, qq);
+    warp_bisect_all(d, e2, ae, m, s == n ? lam : mu + s * (n - 1));
+  }
+  __syncthreads();
+
+  small_identity_phase(lam, mu, n, batch, tol, log_domain, mat, out, lambda_out,
+                       mu_out, status);
+}
+
+// Split form for few matrices (C1): the n+1 solves of matrix blockIdx.y are
+// spread over gridDim.x CTAs (one warp per solve), spectra go to global
+// memory, then small_identity_kernel finishes each matrix.
+__global__ void small_solves_kernel(const double* __restrict__ A, int n,
+                                    double* __restrict__ lam_g,
+                                    double* __restrict__ mu_g) {
+  extern __shared__ double sm[];
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long mat = blockIdx.y;
+  const int s = blockIdx.x * nw + warp;
+  if (s > n) return;
+  const int ld = n | 1;
+  double* S = sm + warp * (n * ld + 5 * n);
+  double* d = S + n * ld;
+  double* e2 = d + n;
+  double* ae = e2 + n;
+  double* uu = ae + n;
+  double* qq = uu + n;
+  const double* Ag = A + mat * (long long)n * n;
+  const int m = (s == n) ? n : n - 1;
+  for (int t = lane; t < m * m; t += 32) {
+    const int r = t / m, c = t % m;
+    const int rr = (s < n && r >= s) ? r + 1 : r;
+    const int cc = (s < n && c >= s) ? c + 1 : c;
+    S[r * ld + c] = Ag[rr * n + cc];
+  }
+  __syncwarp();
+  warp_tridiagonalize(S, ld, m, d, e2, ae, uu, qq);
+  warp_bisect_all(d, e2, ae, m, s == n ? lam_g + mat * n
+                                       : mu_g + (mat * n + s) * (long long)(n - 1));
+}
+
+__global__ void small_identity_kernel(const double* __restrict__ lam_g,
+                                      const double* __restrict__ mu_g, int n,
+                                      int batch, double tol, int log_domain,
+                                      double* __restrict__ out,
+                                      DevStatus* status) {
+  extern __shared__ double sm[];
+  const long long mat = blockIdx.x;
+  double* lam = sm;
+  double* mu = sm + n;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) lam[t] = lam_g[mat * n + t];
+  for (int t = threadIdx.x; t < n * (n - 1); t += blockDim.x)
+    mu[t] = mu_g[mat * (long long)n * (n - 1) + t];
+  __syncthreads();
+  small_identity_phase(lam, mu, n, batch, tol, log_domain, mat, out, nullptr,
+                       nullptr, status);
+}
+
 size_t small_smem_bytes(int n, int warps) {
   const int ldA = n | 1;
   return sizeof(double) *
@@ -234,10 +296,34 @@ size_t small_smem_bytes(int n, int warps) {
 
 int small_warps_for(int n) { return n <= 16 ? 2 : 4; }
 
+cudaError_t launch_small_split(const double* dA, size_t count, int n,
+                               int batch, double tol, int log_domain,
+                               double* dout, double* dlam, double* dmu,
+                               DevStatus* dstatus, cudaStream_t stream) {
+  const int warps = 2;
+  const size_t smem1 = sizeof(double) * (size_t)warps * (n * (n | 1) + 5 * n);
+  cudaError_t e = cudaFuncSetAttribute(small_solves_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem1);
+  if (e != cudaSuccess) return e;
+  dim3 g1((n + 1 + warps - 1) / warps, (unsigned)count);
+  small_solves_kernel<<<g1, warps * 32, smem1, stream>>>(dA, n, dlam, dmu);
+  const size_t smem2 = sizeof(double) * (size_t)(n + n * (n - 1));
+  e = cudaFuncSetAttribute(small_identity_kernel,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  if (e != cudaSuccess) return e;
+  small_identity_kernel<<<(unsigned)count, 256, smem2, stream>>>(
+      dlam, dmu, n, batch, tol, log_domain, dout, dstatus);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_small_all(const double* dA, size_t count, int n, int batch,
                              double tol, int log_domain, double* dout,
                              double* dlam, double* dmu, DevStatus* dstatus,
                              cudaStream_t stream) {
+  if (count * 4 < 148 && dlam && dmu)  // few matrices: spread the solves
+    return launch_small_split(dA, count, n, batch, tol, log_domain, dout, dlam,
+                              dmu, dstatus, stream);
   const int warps = small_warps_for(n);
   const size_t smem = small_smem_bytes(n, warps);
   cudaError_t e = cudaFuncSetAttribute(small_all_magnitudes_kernel,
