@@ -119,7 +119,7 @@ namespace {
 
 constexpr int kSmallMax = 64;
 constexpr int kLargeMax = 14000;  // bisection stages (d, e^2) in shared memory
-constexpr int kStage1Slots = 148;
+constexpr int kStage1Slots = 296;  // two band-reduction CTAs per SM
 
 struct DevBuf {
   void* p = nullptr;

@@ -27,10 +27,12 @@ constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
 // Shared-memory layout (doubles).  One CTA (8 warps) per SM; the GEMM
 // region is reused by the panel / Gram phases.
-constexpr int kG2M = 128, kG2N = 64, kG2K = 2 * kB, kG2LD = kG2K + 4;  // 68
-constexpr int kG2_A = kG2M * kG2LD;                 // Aop  128 x 64
-constexpr int kG2_B = kG2N * kG2LD;                 // Bop   64 x 64 (x2)
-constexpr int kG1M = 128, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 132;
+constexpr int kG2M = 64, kG2N = 32, kG2K = 2 * kB, kG2LD = kG2K + 4;  // 68
+constexpr int kG2_A = kG2M * kG2LD;                 // Aop  64 x 64
+constexpr int kG2_B = kG2N * kG2LD;                 // Bop  32 x 64 (x2)
+constexpr int kG1M = 64, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 68;
+constexpr int kMT1 = kG1M / 32;                     // 8-row m-tiles per warp
+constexpr int kMT2 = kG2M / 32, kNT2 = kG2N / 16;   // GEMM2 warp tile
 constexpr int kG1_A = kG1M * kG1LDA;                // pass 1: A chunk 128 x 32
 constexpr int kG1_T = kG1K * kG1TLD;                // pass 2: A chunk 32 x 128
 constexpr int kG1_B = kG1K * kG1LDB;                // VT chunk 32 x 32
@@ -42,7 +44,10 @@ constexpr int kGemmSmem =
     cmax(cmax(kG2_A + 2 * kG2_B, 2 * (kG1_A + kG1_B)),
          cmax(2 * (kG1_T + kG1_B), kGramPart));
 constexpr int kRed = 8 + 8 * kB;
-constexpr int kStage1SmemDoubles = kGemmSmem + 6 * kSmallMat + kRed + 4 * kB;
+// T, G/Y, A persist across Gram calls; B and R live in the GEMM region
+// (never alive across a gram() or GEMM call).  ~98 KB: two CTAs per SM.
+constexpr int kStage1SmemDoubles = kGemmSmem + 3 * kSmallMat + kRed + 4 * kB;
+static_assert(kGemmSmem >= kGramPart && kGemmSmem >= 2 * kSmallMat, "smem");
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile(
@@ -441,9 +446,9 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
     for (int rb = 0; rb < s; rb += kG1M) {
       const int kend = min(rb + kG1M, s);
       const int nk = (kend + kG1K - 1) / kG1K;
-      double acc[4][2][2];
+      double acc[kMT1][2][2];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < kMT1; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
       auto stage = [&](int kb, int buf) {
@@ -481,17 +486,17 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
 #pragma unroll
         for (int k4 = 0; k4 < kG1K / 4; ++k4) {
           const int kl = 4 * k4 + kk;
-          double af[4], bf[2];
+          double af[kMT1], bf[2];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const int ml = 32 * wm + 8 * mt + mm;
+          for (int mt = 0; mt < kMT1; ++mt) {
+            const int ml = 8 * kMT1 * wm + 8 * mt + mm;
             const double v = a[ml * kG1LDA + kl];
             af[mt] = (diag && kb + kl > rb + ml) ? 0.0 : v;
           }
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) bf[nt] = b[kl * kG1LDB + 16 * wn + 8 * nt + mm];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt)
+          for (int mt = 0; mt < kMT1; ++mt)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
               dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
@@ -499,8 +504,8 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
         __syncthreads();
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int r = rb + 32 * wm + 8 * mt + mm;
+      for (int mt = 0; mt < kMT1; ++mt) {
+        const int r = rb + 8 * kMT1 * wm + 8 * mt + mm;
         if (r >= s) continue;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -520,10 +525,10 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
       const int k0 = cb + 1;  // rows r > c >= cb
       if (k0 >= s) break;
       const int nk = (s - k0 + kG1K - 1) / kG1K;
-      double acc[4][2][2];
+      double acc[kMT1][2][2];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int r = cb + 32 * wm + 8 * mt + mm;
+      for (int mt = 0; mt < kMT1; ++mt) {
+        const int r = cb + 8 * kMT1 * wm + 8 * mt + mm;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           const int c = 16 * wn + 8 * nt + 2 * kk;
@@ -539,7 +544,7 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
       const int cend = min(cb + kG1M, s);
       auto stage = [&](int kb, int buf) {
         for (int t = tid; t < kG1K * (kG1M / 2); t += kNT) {
-          const int r = t >> 6, c2 = (t & 63) * 2;
+          const int r = t / (kG1M / 2), c2 = (t % (kG1M / 2)) * 2;
           const int gr = kb + r, gc = cb + c2;
           int bytes = 0;
           if (gr < s && gc < cend) bytes = (gc + 1 < cend) ? 16 : 8;
@@ -572,17 +577,17 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
 #pragma unroll
         for (int k4 = 0; k4 < kG1K / 4; ++k4) {
           const int kl = 4 * k4 + kk;
-          double af[4], bf[2];
+          double af[kMT1], bf[2];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const int ml = 32 * wm + 8 * mt + mm;
+          for (int mt = 0; mt < kMT1; ++mt) {
+            const int ml = 8 * kMT1 * wm + 8 * mt + mm;
             const double v = a[kl * kG1TLD + ml];
             af[mt] = (diag && kb + kl <= cb + ml) ? 0.0 : v;
           }
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) bf[nt] = b[kl * kG1LDB + 16 * wn + 8 * nt + mm];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt)
+          for (int mt = 0; mt < kMT1; ++mt)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
               dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
@@ -590,8 +595,8 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
         __syncthreads();
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int r = cb + 32 * wm + 8 * mt + mm;
+      for (int mt = 0; mt < kMT1; ++mt) {
+        const int r = cb + 8 * kMT1 * wm + 8 * mt + mm;
         if (r >= s) continue;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -618,13 +623,13 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
   const int wm = warp >> 1, wn = warp & 1;
   double* sOA = sm;
   double* sOB[2] = {sm + kG2_A, sm + kG2_A + kG2_B};
-  auto load_c = [&](int rb, int cb, double (&c)[4][4][2]) {
+  auto load_c = [&](int rb, int cb, double (&c)[kMT2][kNT2][2]) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int r = rb + 32 * wm + 8 * mt + mm;
+    for (int mt = 0; mt < kMT2; ++mt) {
+      const int r = rb + 8 * kMT2 * wm + 8 * mt + mm;
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int col = cb + 32 * wn + 8 * nt + 2 * kk;
+      for (int nt = 0; nt < kNT2; ++nt) {
+        const int col = cb + 8 * kNT2 * wn + 8 * nt + 2 * kk;
         if (r < s && col + 1 < s) {
           // volatile: keeps the prefetch ahead of the (volatile) DMMAs of the
           // current tile instead of letting the scheduler sink it to its use
@@ -640,7 +645,7 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
   };
   auto stage_b = [&](int cb, int buf) {
     for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
-      const int r = t >> 5, k2 = (t & 31) * 2;
+      const int r = t / (kG2K / 2), k2 = (t % (kG2K / 2)) * 2;
       const int gr = cb + r;
       const int bytes = gr < s ? 16 : 0;
       const double* src = k2 < kB ? V + (long long)(bytes ? gr : 0) * kB + k2
@@ -660,16 +665,16 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
     }
     const int cend = min(rb + kG2M, s);
     const int ncb = (cend + kG2N - 1) / kG2N;
-    double cn[4][4][2];
+    double cn[kMT2][kNT2][2];
     load_c(rb, 0, cn);
     stage_b(0, 0);
     for (int ci = 0; ci < ncb; ++ci) {
       const int cb = ci * kG2N;
-      double acc[4][4][2];
+      double acc[kMT2][kNT2][2];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < kMT2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
+        for (int nt = 0; nt < kNT2; ++nt) {
           acc[mt][nt][0] = cn[mt][nt][0];
           acc[mt][nt][1] = cn[mt][nt][1];
         }
@@ -685,24 +690,26 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
 #pragma unroll 4
       for (int k4 = 0; k4 < kG2K / 4; ++k4) {
         const int kl = 4 * k4 + kk;
-        double af[4], bf[4];
+        double af[kMT2], bf[kNT2];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) af[mt] = sOA[(32 * wm + 8 * mt + mm) * kG2LD + kl];
+        for (int mt = 0; mt < kMT2; ++mt)
+          af[mt] = sOA[(8 * kMT2 * wm + 8 * mt + mm) * kG2LD + kl];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) bf[nt] = b[(32 * wn + 8 * nt + mm) * kG2LD + kl];
+        for (int nt = 0; nt < kNT2; ++nt)
+          bf[nt] = b[(8 * kNT2 * wn + 8 * nt + mm) * kG2LD + kl];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < kMT2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt)
+          for (int nt = 0; nt < kNT2; ++nt)
             dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int r = rb + 32 * wm + 8 * mt + mm;
+      for (int mt = 0; mt < kMT2; ++mt) {
+        const int r = rb + 8 * kMT2 * wm + 8 * mt + mm;
         if (r >= s) continue;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int col = cb + 32 * wn + 8 * nt + 2 * kk;
+        for (int nt = 0; nt < kNT2; ++nt) {
+          const int col = cb + 8 * kNT2 * wn + 8 * nt + 2 * kk;
           double* p = A22 + (long long)r * ldw + col;
           if (col + 1 < s)
             *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
@@ -743,7 +750,7 @@ __device__ unsigned long long g_phase_cycles[16];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
+__global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
 #ifdef EIGENID_PHASE_TIMING
   long long t_ph_ = clock64();
   int ph_ = 0;
@@ -752,11 +759,11 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
   double* sgemm = smem;
   double* sT = smem + kGemmSmem;
   double* sG = sT + kSmallMat;   // G, then Y
-  double* sM = sG + kSmallMat;
-  double* sA = sM + kSmallMat;
-  double* sB = sA + kSmallMat;
-  double* sR = sB + kSmallMat;
-  double* red = sR + kSmallMat;
+  double* sA = sG + kSmallMat;
+  double* sM = sA;               // M = T^T Y (A is dead by then)
+  double* sB = sgemm;            // only alive between gram()/GEMM calls
+  double* sR = sgemm + kSmallMat;
+  double* red = sA + kSmallMat;
   double* stau = red + kRed;
   double* wsm = stau + kB;
   double* sS = wsm + kB;
