@@ -119,7 +119,7 @@ namespace {
 
 constexpr int kSmallMax = 64;
 constexpr int kLargeMax = 14000;  // bisection stages (d, e^2) in shared memory
-constexpr int kStage1Slots = 148;  // one band-reduction CTA per SM
+constexpr int kStage1Slots = 296;  // two band-reduction CTAs per SM
 
 struct DevBuf {
   void* p = nullptr;
@@ -302,7 +302,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   const int kB = stage1_bandwidth();
   const int ldab = stage1_band_ld();
   const int ldw = (n + 7) & ~7;
-  const long long ws_stride = (long long)n * ldw + 5LL * n * kB;
+  const long long ws_stride = (long long)n * ldw + 3LL * n * kB;
   const int slots = nsolves < kStage1Slots ? nsolves : kStage1Slots;
   int launches = 0;
   EID_CUDA(c->bJs.ensure(sizeof(int) * (size_t)nsolves), "alloc js");

@@ -27,10 +27,10 @@ constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
 // Shared-memory layout (doubles).  One CTA (8 warps) per SM; the GEMM
 // region is reused by the panel / Gram phases.
-constexpr int kG2M = 128, kG2N = 32, kG2K = 2 * kB, kG2LD = kG2K + 4;  // 68
-constexpr int kG2_A = kG2M * kG2LD;                 // Aop  128 x 64
-constexpr int kG2_B = kG2N * kG2LD;                 // Bop   32 x 64 (x2)
-constexpr int kG1M = 128, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 132;
+constexpr int kG2M = 64, kG2N = 32, kG2K = 2 * kB, kG2LD = kG2K + 4;  // 68
+constexpr int kG2_A = kG2M * kG2LD;                 // Aop  64 x 64
+constexpr int kG2_B = kG2N * kG2LD;                 // Bop  32 x 64 (x2)
+constexpr int kG1M = 64, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 68;
 constexpr int kMT1 = kG1M / 32;                     // 8-row m-tiles per warp
 constexpr int kMT2 = kG2M / 32, kNT2 = kG2N / 16;   // GEMM2 warp tile
 constexpr int kG1_A = kG1M * kG1LDA;                // pass 1: A chunk 128 x 32
@@ -40,17 +40,12 @@ constexpr int kSmallLD = kB + 1;
 constexpr int kSmallMat = kB * kSmallLD;            // T, G/Y, M
 constexpr int kGramPart = 8 * kSmallMat;
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
-// fused SYR2K(p) + SYMM(p+1) tile: Aop 128x64, Bop 32x64 (x2), C 128x32,
-// VT rows of the row block 128x32, VT rows of the column block 32x32 (x2)
-constexpr int kFC = kG2M * kG1LDA, kFVc = kB * kG1LDB;
-constexpr int kFusedSmem = kG2_A + 2 * kG2_B + kFC + kFC + 2 * kFVc;
 constexpr int kGemmSmem =
-    cmax(cmax(cmax(kG2_A + 2 * kG2_B, 2 * (kG1_A + kG1_B)),
-              cmax(2 * (kG1_T + kG1_B), kGramPart)),
-         kFusedSmem);
+    cmax(cmax(kG2_A + 2 * kG2_B, 2 * (kG1_A + kG1_B)),
+         cmax(2 * (kG1_T + kG1_B), kGramPart));
 constexpr int kRed = 8 + 8 * kB;
 // T, G/Y, A persist across Gram calls; B and R live in the GEMM region
-// (never alive across a gram() or GEMM call).  ~220 KB: one CTA per SM.
+// (never alive across a gram() or GEMM call).  ~98 KB: two CTAs per SM.
 constexpr int kStage1SmemDoubles = kGemmSmem + 3 * kSmallMat + kRed + 4 * kB;
 static_assert(kGemmSmem >= kGramPart && kGemmSmem >= 2 * kSmallMat, "smem");
 
@@ -622,7 +617,7 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
 // ahead.  Tiles crossing the diagonal also write their (never read) upper
 // part.
 __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
-                      const double* V, double* sm, int col_limit) {
+                      const double* V, double* sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
   const int wm = warp >> 1, wn = warp & 1;
@@ -668,7 +663,7 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
       if (gr < s) v = k < kB ? W2[(long long)gr * kB + k] : V[(long long)gr * kB + k - kB];
       sOA[r * kG2LD + k] = -v;
     }
-    const int cend = min(min(rb + kG2M, s), col_limit);
+    const int cend = min(rb + kG2M, s);
     const int ncb = (cend + kG2N - 1) / kG2N;
     double cn[kMT2][kNT2][2];
     load_c(rb, 0, cn);
@@ -728,221 +723,6 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
   __syncthreads();
 }
 
-// ---- fused: SYR2K of panel p and SYMM of panel p+1 in one pass ----------
-// A22n = trailing matrix of panel p+1 (= A22_p shifted by 32 rows/cols).
-// For every lower tile (128 rows x 32 cols): C = A22n tile
-//   C -= W2_p V_p^T + V_p W2_p^T        (the rest of panel p's update)
-//   store C;  X[rb] += tril(C) VTn[cb];  X[cb] += strict(C)^T VTn[rb]
-// so the trailing matrix is read and written once per panel instead of
-// being read three times and written once (X must be zero on entry).
-__device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
-                           const double* Vp, const double* VTn, double* Xn,
-                           double* sm) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kk = lane & 3, mm = lane >> 2;
-  const int wm = warp >> 1, wn = warp & 1;
-  double* sOA = sm;
-  double* sOB[2] = {sm + kG2_A, sm + kG2_A + kG2_B};
-  double* sC = sm + kG2_A + 2 * kG2_B;
-  double* sVr = sC + kFC;
-  double* sVc[2] = {sVr + kFC, sVr + kFC + kFVc};
-  auto load_c = [&](int rb, int cb, double (&c)[4][2][2]) {
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int r = rb + 32 * wm + 8 * mt + mm;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int col = cb + 16 * wn + 8 * nt + 2 * kk;
-        if (r < sn && col + 1 < sn) {
-          asm volatile("ld.global.v2.f64 {%0, %1}, [%2];\n"
-                       : "=d"(c[mt][nt][0]), "=d"(c[mt][nt][1])
-                       : "l"(A22n + (long long)r * ldw + col));
-        } else {
-          c[mt][nt][0] = (r < sn && col < sn) ? A22n[(long long)r * ldw + col] : 0.0;
-          c[mt][nt][1] = 0.0;
-        }
-      }
-    }
-  };
-  auto stage_tile = [&](int cb, int buf) {
-    // Bop rows of panel p (shifted by 32): [V_p | W2_p]
-    for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
-      const int r = t / (kG2K / 2), k2 = (t % (kG2K / 2)) * 2;
-      const int gr = cb + r;
-      const int bytes = gr < sn ? 16 : 0;
-      const long long row = 32 + (bytes ? gr : 0);
-      const double* src = k2 < kB ? Vp + row * kB + k2 : W2p + row * kB + (k2 - kB);
-      cp_async16(sOB[buf] + r * kG2LD + k2, src, bytes);
-    }
-    // VT of panel p+1, rows cb..cb+31
-    for (int t = tid; t < kB * (kB / 2); t += kNT) {
-      const int r = t >> 4, c2 = (t & 15) * 2;
-      const int gr = cb + r;
-      const int bytes = gr < sn ? 16 : 0;
-      cp_async16(sVc[buf] + r * kG1LDB + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
-                 bytes);
-    }
-    cpa_commit();
-  };
-  for (int rb = 0; rb < sn; rb += kG2M) {
-    __syncthreads();
-    for (int t = tid; t < kG2M * kG2K; t += kNT) {
-      const int r = t / kG2K, k = t % kG2K;
-      const int gr = rb + r;
-      double v = 0.0;
-      if (gr < sn)
-        v = k < kB ? W2p[(long long)(32 + gr) * kB + k] : Vp[(long long)(32 + gr) * kB + k - kB];
-      sOA[r * kG2LD + k] = -v;
-    }
-    for (int t = tid; t < kG2M * (kB / 2); t += kNT) {
-      const int r = t >> 4, c2 = (t & 15) * 2;
-      const int gr = rb + r;
-      const int bytes = gr < sn ? 16 : 0;
-      cp_async16(sVr + r * kG1LDB + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2, bytes);
-    }
-    cpa_commit();
-    double xacc[4][2][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) xacc[a][b][0] = xacc[a][b][1] = 0.0;
-    const int cend = min(rb + kG2M, sn);
-    const int ncb = (cend + kB - 1) / kB;
-    double cn[4][2][2];
-    load_c(rb, 0, cn);
-    stage_tile(0, 0);
-    for (int ci = 0; ci < ncb; ++ci) {
-      const int cb = ci * kB;
-      double acc[4][2][2];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          acc[mt][nt][0] = cn[mt][nt][0];
-          acc[mt][nt][1] = cn[mt][nt][1];
-        }
-      if (ci + 1 < ncb) {
-        load_c(rb, cb + kB, cn);
-        stage_tile(cb + kB, (ci + 1) & 1);
-        cpa_wait1();
-      } else {
-        cpa_wait0();
-      }
-      __syncthreads();
-      // ---- SYR2K part: acc += -[W2|V](rb) [V|W2](cb)^T
-      const double* b = sOB[ci & 1];
-#pragma unroll 4
-      for (int k4 = 0; k4 < kG2K / 4; ++k4) {
-        const int kl = 4 * k4 + kk;
-        double af[4], bf[2];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) af[mt] = sOA[(32 * wm + 8 * mt + mm) * kG2LD + kl];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) bf[nt] = b[(16 * wn + 8 * nt + mm) * kG2LD + kl];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-            dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-      }
-      // store C (global, lower part and the crossing tile) and stage it
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int rl = 32 * wm + 8 * mt + mm;
-        const int r = rb + rl;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int cl = 16 * wn + 8 * nt + 2 * kk;
-          const int col = cb + cl;
-          *reinterpret_cast<double2*>(sC + rl * kG1LDA + cl) =
-              make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-          if (r < sn) {
-            double* p = A22n + (long long)r * ldw + col;
-            if (col + 1 < sn)
-              *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-            else if (col < sn)
-              p[0] = acc[mt][nt][0];
-          }
-        }
-      }
-      __syncthreads();
-      const bool diag = cb + kB > rb;  // tile crosses the diagonal
-      const double* vc = sVc[ci & 1];
-      // ---- SYMM part 1: X[rb] += tril(C) VT[cb]   (K = 32)
-#pragma unroll
-      for (int k4 = 0; k4 < kB / 4; ++k4) {
-        const int kl = 4 * k4 + kk;
-        double af[4], bf[2];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          const int ml = 32 * wm + 8 * mt + mm;
-          const double v = sC[ml * kG1LDA + kl];
-          af[mt] = (diag && cb + kl > rb + ml) ? 0.0 : v;
-        }
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) bf[nt] = vc[kl * kG1LDB + 16 * wn + 8 * nt + mm];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-            dmma(xacc[mt][nt][0], xacc[mt][nt][1], af[mt], bf[nt]);
-      }
-      // ---- SYMM part 2: X[cb] += strict(C)^T VT[rb]   (32 x 32, K = 128)
-      {
-        const int mt2 = warp >> 1, nb2 = 2 * (warp & 1);
-        double x2[2][2];
-        const int xr = cb + 8 * mt2 + mm;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int xc = 8 * (nb2 + q) + 2 * kk;
-          if (xr < sn) {
-            const double2 t = *reinterpret_cast<const double2*>(Xn + (long long)xr * kB + xc);
-            x2[q][0] = t.x;
-            x2[q][1] = t.y;
-          } else {
-            x2[q][0] = x2[q][1] = 0.0;
-          }
-        }
-#pragma unroll 8
-        for (int k4 = 0; k4 < kG2M / 4; ++k4) {
-          const int kl = 4 * k4 + kk;         // row of C
-          const int ml = 8 * mt2 + mm;        // column of C
-          const double v = sC[kl * kG1LDA + ml];
-          const double af = (diag && rb + kl <= cb + ml) ? 0.0 : v;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const double bv = sVr[kl * kG1LDB + 8 * (nb2 + q) + mm];
-            dmma(x2[q][0], x2[q][1], af, bv);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int xc = 8 * (nb2 + q) + 2 * kk;
-          if (xr < sn)
-            *reinterpret_cast<double2*>(Xn + (long long)xr * kB + xc) =
-                make_double2(x2[q][0], x2[q][1]);
-        }
-      }
-      __syncthreads();
-    }
-    // X[rb] += register accumulation (rows of this block may already hold
-    // transposed contributions from its diagonal tiles)
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int r = rb + 32 * wm + 8 * mt + mm;
-      if (r >= sn) continue;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int c = 16 * wn + 8 * nt + 2 * kk;
-        double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + c);
-        const double2 t = *p;
-        *p = make_double2(t.x + xacc[mt][nt][0], t.y + xacc[mt][nt][1]);
-      }
-    }
-  }
-  __syncthreads();
-}
-
 __device__ void write_band(const double* W, int ldw, int m, int c_begin,
                            int c_end, double* band) {
   for (int t = threadIdx.x; t < (c_end - c_begin) * kLDAB; t += kNT) {
@@ -970,7 +750,7 @@ __device__ unsigned long long g_phase_cycles[16];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
+__global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
 #ifdef EIGENID_PHASE_TIMING
   long long t_ph_ = clock64();
   int ph_ = 0;
@@ -991,36 +771,9 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = args.n, ldw = args.ldw;
   double* W = args.ws + blockIdx.x * args.ws_stride;
-  double* Vbuf[2] = {W + (long long)n * ldw, W + (long long)n * ldw + (long long)n * kB};
-  double* VTg = Vbuf[1] + (long long)n * kB;
-  double* Xbuf[2] = {VTg + (long long)n * kB, VTg + 2LL * n * kB};
-
-  // Householder representation (V, T) of the panel P0 (s x kB, ld ldw) and
-  // VT = V T; Xs is scratch.
-  auto factor = [&](double* P0, int s, double* Vg, double* Xs) {
-    const bool fast = s >= 2 * kB &&
-                      chol_panel(P0, ldw, s, Vg, Xs, sT, sG, sA, sB, sR, sS, sgemm,
-                                 sflag);
-    if (!fast) {
-      panel_qr(P0, ldw, s, stau, red, wsm);
-      extract_v(P0, ldw, s, Vg);
-      gram(Vg, kB, Vg, kB, s, sG, sgemm);  // T (dlarft) from G = V^T V
-      if (warp == 0) {
-        for (int t = 0; t < kB; ++t) {
-          double v = 0.0;
-          if (lane < t)
-            for (int p = lane; p < t; ++p) v += sT[lane * kSmallLD + p] * sG[p * kSmallLD + t];
-          __syncwarp();
-          if (lane < t) sT[lane * kSmallLD + t] = -stau[t] * v;
-          if (lane == t) sT[t * kSmallLD + t] = stau[t];
-          if (lane > t) sT[lane * kSmallLD + t] = 0.0;
-          __syncwarp();
-        }
-      }
-    }
-    __syncthreads();
-    row_transform(Vg, kB, sT, 1.0, nullptr, VTg, s);   // VT = V T
-  };
+  double* Vg = W + (long long)n * ldw;
+  double* VTg = Vg + (long long)n * kB;
+  double* Xg = VTg + (long long)n * kB;
 
   for (int sidx = blockIdx.x; sidx < args.nsolves; sidx += gridDim.x) {
     const int j = args.js[sidx];
@@ -1045,53 +798,55 @@ __global__ void __launch_bounds__(kNT, 1) band_reduce_kernel(Stage1Args args) {
       }
     }
     __syncthreads();
-    int c = 0, par = 0;
-    int s = m - kB;
-    if (s >= 2) {
+    int c = 0;
+    for (; c < m; c += kB) {
+      const int s = m - c - kB;
+      if (s < 2) break;
+      const int c0 = c + kB;
+      double* P0 = W + (long long)c0 * ldw + c;
       PHASE(2);
-      factor(W + (long long)kB * ldw, s, Vbuf[0], Xbuf[0]);
-      write_band(W, ldw, m, 0, kB, band);
+      const bool fast = s >= 2 * kB &&
+                        chol_panel(P0, ldw, s, Vg, Xg, sT, sG, sA, sB, sR, sS,
+                                   sgemm, sflag);
+      if (!fast) {
+        panel_qr(P0, ldw, s, stau, red, wsm);
+        extract_v(P0, ldw, s, Vg);
+        // T (dlarft, forward columnwise) from G = V^T V
+        gram(Vg, kB, Vg, kB, s, sG, sgemm);
+        if (warp == 0) {
+          for (int t = 0; t < kB; ++t) {
+            double v = 0.0;
+            if (lane < t)
+              for (int p = lane; p < t; ++p) v += sT[lane * kSmallLD + p] * sG[p * kSmallLD + t];
+            __syncwarp();
+            if (lane < t) sT[lane * kSmallLD + t] = -stau[t] * v;
+            if (lane == t) sT[t * kSmallLD + t] = stau[t];
+            if (lane > t) sT[lane * kSmallLD + t] = 0.0;
+            __syncwarp();
+          }
+        }
+      }
+      __syncthreads();
+      PHASE(3);
+      write_band(W, ldw, m, c, c + kB, band);
+      row_transform(Vg, kB, sT, 1.0, nullptr, VTg, s);       // VT = V T
+      double* A22 = W + (long long)c0 * ldw + c0;
       PHASE(4);
-      gemm1(W + (long long)kB * ldw + kB, ldw, s, VTg, Xbuf[0], sgemm);  // X = A22 VT
-    }
-    while (s >= 2) {
-      double* Vc = Vbuf[par];
-      double* Xc = Xbuf[par];
-      double* A22 = W + (long long)(c + kB) * ldw + (c + kB);
+      gemm1(A22, ldw, s, VTg, Xg, sgemm);                     // X = A22 VT
       PHASE(5);
-      gram(Vc, kB, Xc, kB, s, sG, sgemm);                    // Y = V^T X
-      for (int t = tid; t < kB * kB; t += kNT) {             // M = T^T Y
+      gram(Vg, kB, Xg, kB, s, sG, sgemm);                     // Y = V^T X
+      for (int t = tid; t < kB * kB; t += kNT) {              // M = T^T Y
         const int q = t / kB, p = t % kB;
         double v = 0.0;
         for (int u = 0; u <= q; ++u) v += sT[u * kSmallLD + q] * sG[u * kSmallLD + p];
         sM[q * kSmallLD + p] = v;
       }
       __syncthreads();
-      row_transform(Vc, kB, sM, -0.5, Xc, Xc, s);            // W2 = X - V M/2
-      const int sn = s - kB;
-      if (sn >= 2) {
-        // look-ahead: update the next panel's columns, factor it, then one
-        // fused pass finishes panel c's update and forms X for panel c+kB
-        PHASE(6);
-        gemm2(A22, ldw, s, Xc, Vc, sgemm, kB);
-        PHASE(2);
-        double* Vn = Vbuf[par ^ 1];
-        double* Xn = Xbuf[par ^ 1];
-        factor(A22 + (long long)kB * ldw, sn, Vn, Xn);
-        write_band(W, ldw, m, c + kB, c + 2 * kB, band);
-        for (int t = tid; t < sn * kB; t += kNT) Xn[t] = 0.0;
-        __syncthreads();
-        PHASE(7);
-        gemm_fused(A22 + (long long)kB * ldw + kB, ldw, sn, Xc, Vc, VTg, Xn, sgemm);
-        par ^= 1;
-      } else {
-        PHASE(6);
-        gemm2(A22, ldw, s, Xc, Vc, sgemm, s);                // last update
-      }
-      c += kB;
-      s = sn;
+      row_transform(Vg, kB, sM, -0.5, Xg, Xg, s);             // W2 = X - V M/2
+      PHASE(6);
+      gemm2(A22, ldw, s, Xg, Vg, sgemm);                      // A22 -= W2V^T+VW2^T
+      PHASE(7);
     }
-    PHASE(3);
     write_band(W, ldw, m, c, m, band);
     __syncthreads();
   }

@@ -18,7 +18,7 @@ eng = IdentityEngine()
 lam, mu = eng.minor_spectra(a, 0, rows)
 buf = (ctypes.c_ulonglong * 16)()
 lib.eigenid_debug_phase_cycles(buf)
-names = ['other', 'copy', 'factor+VT', 'final band', 'gemm1 (first)', 'Y,M,W2', 'gemm2 strip', 'fused']
+names = ['other', 'copy', 'panel', 'band+VT', 'gemm1', 'Y,M,W2', 'gemm2', '-']
 tot = sum(buf[i] for i in range(8))
 print('stage 1 (CTA 0):')
 for i in range(8): print(f'  {names[i]:10s} {buf[i]/1.965e9*1e3:9.2f} ms  {100*buf[i]/max(tot,1):5.1f}%')
