@@ -100,24 +100,101 @@ __device__ __forceinline__ double pow2_scale(double tn) {
   return scalbn(1.0, -(ilogb(tn) + 1));
 }
 
-// Bisects eigenvalue k (0-based, ascending) of the scaled (d, e2) inside
-// [lo, hi) with count(lo) <= k < count(hi) already established.  Stops at
+// Sturm count plus the determinant det(T - x) = p * 2^e of the same
+// division-free recurrence (sign(det) = (-1)^count); used for the secant
+// (Illinois) acceleration of bisection.
+__device__ __forceinline__ int sturm_det(const double* __restrict__ d,
+                                         const double* __restrict__ e2, int m,
+                                         double x, double* pdet, int* edet) {
+  double p0 = 1.0, p1 = d[0] - x;
+  if (p1 == 0.0) p1 = -0x1p-900;
+  int cnt = __double2hiint(p1) < 0;
+  int ex = 0;
+  int k = 1;
+  for (; k + 4 <= m; k += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double p2 = fma(d[k + u] - x, p1, -e2[k + u - 1] * p0);
+      if (p2 == 0.0) p2 = -p1 * 0x1p-900;
+      cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+      p0 = p1;
+      p1 = p2;
+    }
+    const double mx = fmax(fabs(p0), fabs(p1));
+    if (mx > 0x1p256 || mx < 0x1p-256) {
+      const int sh = ilogb(mx);
+      const double f = scalbn(1.0, -sh);
+      p0 *= f;
+      p1 *= f;
+      ex += sh;
+    }
+  }
+  for (; k < m; ++k) {
+    double p2 = fma(d[k] - x, p1, -e2[k - 1] * p0);
+    if (p2 == 0.0) p2 = -p1 * 0x1p-900;
+    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+    p0 = p1;
+    p1 = p2;
+  }
+  *pdet = p1;
+  *edet = ex;
+  return cnt;
+}
+
+// Eigenvalue k (0-based, ascending) of the scaled (d, e2) inside [lo, hi)
+// with count(lo) <= k < count(hi).  Bisection until the bracket isolates
+// eigenvalue k (count(lo) == k, count(hi) == k+1), then Illinois-modified
+// regula falsi on det(T - x), which has exactly one sign change there; every
+// trial point still updates the bracket by its Sturm count, so the result is
+// the same eigenvalue bisection would find.  Stops at
 // hi - lo <= max(atol, 2 eps max(|lo|,|hi|)) — the accuracy the
 // Householder reduction's backward error (~eps ||T||) supports.
 __device__ __forceinline__ double bisect_one(const double* __restrict__ d,
                                              const double* __restrict__ e2,
                                              int m, int k, double lo, double hi,
                                              double atol) {
-  for (int it = 0; it < 200; ++it) {
+  double plo, phi;
+  int elo, ehi;
+  int clo = sturm_det(d, e2, m, lo, &plo, &elo);
+  int chi = sturm_det(d, e2, m, hi, &phi, &ehi);
+  int side = 0;
+  for (int it = 0; it < 300; ++it) {
     const double w = hi - lo;
     const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
     if (w <= tol) break;
-    const double mid = lo + 0.5 * w;
-    if (mid <= lo || mid >= hi) break;
-    if (sturm_count(d, e2, m, mid) > k)
-      hi = mid;
-    else
-      lo = mid;
+    double x = lo + 0.5 * w;
+    // secant step when eigenvalue k is isolated; every third step bisects
+    // (safeguard), and secant points are kept 1% inside the bracket
+    if (clo == k && chi == k + 1 && it % 3 != 2) {
+      const int de = ehi - elo;
+      double r = phi / plo;
+      r = de > 1000 ? -1e300 : (de < -1000 ? -1e-300 : scalbn(r, de));
+      const double xs = lo + w / (1.0 - r);
+      const double g = 0.01 * w;
+      x = fmin(fmax(xs, lo + g), hi - g);
+      if (!(x > lo && x < hi)) x = lo + 0.5 * w;
+    } else {
+      side = 0;
+    }
+    if (!(x > lo && x < hi)) break;  // interval is a few ulps wide
+    double px;
+    int ex;
+    const int cx = sturm_det(d, e2, m, x, &px, &ex);
+    if (cx > k) {
+      hi = x;
+      phi = px;
+      ehi = ex;
+      chi = cx;
+      if (side == 1) plo *= 0.5;  // Illinois: retained end twice
+      side = 1;
+    } else {
+      lo = x;
+      plo = px;
+      elo = ex;
+      clo = cx;
+      if (side == -1) phi *= 0.5;
+      side = -1;
+    }
   }
   return lo + 0.5 * (hi - lo);
 }
