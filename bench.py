@@ -46,16 +46,17 @@ UNIT = "components/s"
 
 # ----------------------------------------------------------------- inputs
 def goe_matrix(n: int, seed: int = 42) -> np.ndarray:
-    """random_symmetric(seed, n).scaled(sqrt(2/n)) — SURVEY §8 d4."""
-    from oracle.oracle import Oracle  # seeded generator restated from matrix_io.cpp
-    return Oracle().random_symmetric(seed, n) * math.sqrt(2.0 / n)
+    """random_symmetric(seed, n).scaled(sqrt(2/n)) — SURVEY §8 d4 (the
+    reference's seeded generator, provided by the product library)."""
+    from paper_2002_04989_b200 import random_symmetric
+    return random_symmetric(seed, n) * math.sqrt(2.0 / n)
 
 
 def c3_matrix(n: int = 1024, seed: int = 3) -> np.ndarray:
     """A = Q diag(linspace(-1,1)) Q^T, Q from QR of a seeded Gaussian, sign-fixed
     by diag(R), then build(kSymmetrize)."""
-    from oracle.oracle import Oracle
-    g = Oracle().gaussian_stream(seed, n * n).reshape(n, n)
+    from paper_2002_04989_b200.engine import seeded_draws
+    g = seeded_draws(seed, n * n).reshape(n, n)
     q, r = np.linalg.qr(g)
     q = q * np.sign(np.diag(r))[None, :]
     lam = -1.0 + 2.0 * np.arange(n) / (n - 1)
@@ -334,9 +335,10 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
 
     # ---- inputs in HBM
     lam_host = mu_host = None
+    from paper_2002_04989_b200 import random_symmetric
+    from paper_2002_04989_b200.engine import c5_lambda
     if wl in ("C1", "C3", "C4"):
-        a_host = {"C1": lambda: __import__("oracle.oracle", fromlist=["Oracle"]).Oracle()
-                  .random_symmetric(1, 64),
+        a_host = {"C1": lambda: random_symmetric(1, 64),
                   "C3": lambda: c3_matrix(1024), "C4": lambda: goe_matrix(4096)}[wl]()
         a_dev = torch.from_numpy(a_host).to(f"cuda:{dist.local}")
         j0, j1 = shard_range(n, world, rank)
@@ -356,11 +358,9 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
                     full = gather_rows(out_dev, n, world, dist.pg)
         flops = f_tri(n, rows) + f_id(n, rows)
     elif wl == "C2":
-        from oracle.oracle import Oracle
-        orc = Oracle()
         count = 4096
         b0, b1 = shard_range(count, world, rank)
-        a_host = np.stack([orc.random_symmetric(b, 32) for b in range(b0, b1)])
+        a_host = np.stack([random_symmetric(b, 32) for b in range(b0, b1)])
         a_dev = torch.from_numpy(a_host).to(f"cuda:{dist.local}")
         out_dev = torch.empty((b1 - b0, 32 * 32), dtype=torch.float64, device=a_dev.device)
         units = count * 32 * 32
@@ -370,9 +370,7 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
         rows = n
         flops = (b1 - b0) * (f_tri(32, 32) + f_id(32, 32))
     else:  # C5
-        from oracle.oracle import Oracle
-        orc = Oracle()
-        lam_host = orc.c5_lambda(5, n)
+        lam_host = c5_lambda(5, n)
         lam_dev = torch.from_numpy(lam_host).to(f"cuda:{dist.local}")
         j0, j1 = shard_range(n, world, rank)
         rows = j1 - j0

@@ -113,6 +113,26 @@ int eigenid_gpu_identity(eigenid_gpu_ctx* ctx, const double* lambda,
                          const eigenid_gpu_config* cfg, double* out,
                          eigenid_gpu_err* err);
 
+/* One eigenvector's component magnitudes |v_ij|^2, j = 0..n-1
+ * (IdentityEngine::vector_magnitudes, identity.cpp:276-292): n+1 solves.
+ * out: n values; out_raw (nullable): pre-clamp values. */
+int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* ctx, const double* a,
+                                  size_t n, size_t i,
+                                  const eigenid_gpu_config* cfg, double* out,
+                                  double* out_raw, eigenid_gpu_err* err);
+
+/* One component (IdentityEngine::component_magnitude, identity.cpp:240-251;
+ * log_domain_magnitude :253-274 when cfg->log_domain).  Cached spectra are
+ * used when both lambda (n) and mu_j (n-1) are given (no solves); otherwise
+ * lambda(A) and the spectrum of M_j are solved on the device (2 solves).
+ * method: 1 batched, 3 log-domain (EvaluationMethod). */
+int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* ctx, const double* a,
+                                    size_t n, size_t i, size_t j,
+                                    const double* lambda, const double* mu_j,
+                                    const eigenid_gpu_config* cfg,
+                                    double* value, double* raw, int* method,
+                                    eigenid_gpu_err* err);
+
 /* Reference-style per-call instrumentation: eigenvalue solves performed by
  * this context (identity.hpp:137-144).  all_magnitudes adds n+1. */
 size_t eigenid_gpu_solve_count(eigenid_gpu_ctx* ctx);
@@ -149,6 +169,16 @@ int eigenid_gpu_identity_device(eigenid_gpu_ctx* ctx, const double* d_lambda,
 int eigenid_gpu_c5_mu_device(eigenid_gpu_ctx* ctx, uint64_t seed,
                              const double* d_lambda, size_t n, size_t j0,
                              size_t j1, double* d_mu, eigenid_gpu_err* err);
+
+/* random_symmetric (proj/src/matrix_io.cpp:171-181, host): n*n draws of a
+ * seeded mt19937_64 — Box-Muller Gaussian (uniform = 0) or uniform(-1,1)
+ * (uniform = 1) — symmetrised as build(kSymmetrize) does; bit-identical to the
+ * reference.  The seeded input generator of the benchmark configs. */
+void eigenid_random_symmetric(uint64_t seed, size_t n, int uniform,
+                              double* out);
+/* The raw SeededDraws stream (matrix_io.cpp:44-65): `count` Gaussian
+ * (kind 0) or uniform(-1,1) (kind 1) draws. */
+void eigenid_seeded_draws(uint64_t seed, size_t count, int kind, double* out);
 
 /* Number of kernels this context has launched (instrumentation for the
  * bench's gpu_launches field). */

@@ -11,10 +11,11 @@ from .errors import (AsymmetricInput, ConfigError, ConvergenceFailure,  # noqa: 
                      IndexOutOfRange, InternalInconsistency, MatrixTooSmall,
                      NonFiniteEntry, NonFiniteIntermediate)
 from .engine import (Device, IdentityConfig, IdentityEngine,  # noqa: F401
-                     SymmetricMatrix, eigenvalues)
+                     SymmetricMatrix, eigenvalues, random_symmetric)
 
 __all__ = [
     "IdentityEngine", "IdentityConfig", "SymmetricMatrix", "eigenvalues", "Device",
+    "random_symmetric",
     "Error", "MatrixTooSmall", "DegenerateEigenvalue", "ConvergenceFailure",
     "NonFiniteIntermediate", "InternalInconsistency", "ConfigError",
     "IndexOutOfRange", "DeviceError", "AsymmetricInput", "NonFiniteEntry",

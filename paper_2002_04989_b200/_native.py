@@ -48,6 +48,14 @@ SIGNATURES = {
     "eigenid_gpu_identity": (C.c_int, [C.c_void_p, _dp, _dp, C.c_size_t, C.c_size_t,
                                        C.c_size_t, C.POINTER(GpuConfig), _dp,
                                        C.POINTER(GpuErr)]),
+    "eigenid_gpu_vector_magnitudes": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t,
+                                                C.POINTER(GpuConfig), _dp, _dp,
+                                                C.POINTER(GpuErr)]),
+    "eigenid_gpu_component_magnitude": (C.c_int, [C.c_void_p, _dp, C.c_size_t,
+                                                  C.c_size_t, C.c_size_t, _dp, _dp,
+                                                  C.POINTER(GpuConfig), _dp, _dp,
+                                                  C.POINTER(C.c_int),
+                                                  C.POINTER(GpuErr)]),
     "eigenid_gpu_solve_count": (C.c_size_t, [C.c_void_p]),
     "eigenid_gpu_reset_solve_count": (None, [C.c_void_p]),
     "eigenid_gpu_all_magnitudes_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t,
@@ -68,6 +76,8 @@ SIGNATURES = {
                                            C.c_size_t, C.c_size_t, C.c_size_t,
                                            C.c_void_p, C.POINTER(GpuErr)]),
     "eigenid_gpu_launch_count": (C.c_uint64, [C.c_void_p]),
+    "eigenid_random_symmetric": (None, [C.c_uint64, C.c_size_t, C.c_int, _dp]),
+    "eigenid_seeded_draws": (None, [C.c_uint64, C.c_size_t, C.c_int, _dp]),
     "eigenid_gpu_set_profiling": (None, [C.c_void_p, C.c_int]),
     "eigenid_gpu_stage_times": (C.c_int, [C.c_void_p, _dp, C.c_int]),
 }

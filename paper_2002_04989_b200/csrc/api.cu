@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
+#include <random>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -45,6 +47,13 @@ cudaError_t launch_degeneracy(const double* dlam, int n, double tol,
                               int* launches);
 cudaError_t launch_c5_mu(uint64_t seed, const double* dlam, int n, int j0,
                          int rows, double* dmu, cudaStream_t st, int* launches);
+cudaError_t launch_component(const double* dlam, const double* dmu, int n,
+                             int i, int batch, double tol, int log_domain,
+                             double* dout3, DevStatus* dstatus, cudaStream_t st,
+                             int* launches);
+cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
+                          int batch, double* draw, DevStatus* dstatus,
+                          cudaStream_t st, int* launches);
 // band.cu
 struct Stage1Args {
   const double* A;
@@ -430,7 +439,59 @@ int check_n(size_t n, eigenid_gpu_err* err) {
 
 }  // namespace
 
+namespace {
+// SeededDraws (matrix_io.cpp:39-71): std::mt19937_64 and the hand-written
+// variate transforms, so inputs are bit-identical to the reference's.
+struct SeededDraws {
+  std::mt19937_64 gen;
+  bool have_spare = false;
+  double spare = 0.0;
+  explicit SeededDraws(uint64_t seed) : gen(seed) {}
+  double unit() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+  double uniform_open() {
+    for (;;) {
+      const double v = 2.0 * unit() - 1.0;
+      if (v > -1.0) return v;
+    }
+  }
+  double gaussian() {
+    if (have_spare) {
+      have_spare = false;
+      return spare;
+    }
+    double u1 = unit();
+    const double u2 = unit();
+    while (u1 <= 0.0) u1 = unit();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 2.0 * M_PI * u2;
+    spare = r * std::sin(theta);
+    have_spare = true;
+    return r * std::cos(theta);
+  }
+};
+}  // namespace
+
 extern "C" {
+
+void eigenid_random_symmetric(uint64_t seed, size_t n, int uniform, double* e) {
+  SeededDraws d(seed);
+  for (size_t t = 0; t < n * n; ++t) e[t] = uniform ? d.uniform_open() : d.gaussian();
+  double asym = 0.0;  // build(kSymmetrize), matrix.cpp:20-36
+  for (size_t r = 0; r < n; ++r)
+    for (size_t c = r + 1; c < n; ++c) asym = std::fmax(asym, std::fabs(e[r * n + c] - e[c * n + r]));
+  if (asym > 0.0)
+    for (size_t r = 0; r < n; ++r)
+      for (size_t c = r + 1; c < n; ++c) {
+        const double m = 0.5 * (e[r * n + c] + e[c * n + r]);
+        e[r * n + c] = m;
+        e[c * n + r] = m;
+      }
+}
+
+void eigenid_seeded_draws(uint64_t seed, size_t count, int kind, double* out) {
+  SeededDraws d(seed);
+  for (size_t t = 0; t < count; ++t) out[t] = kind ? d.uniform_open() : d.gaussian();
+}
 
 int eigenid_gpu_abi_version(void) { return EIGENID_B200_ABI_VERSION; }
 
@@ -772,6 +833,107 @@ int eigenid_gpu_all_magnitudes_batched_device(eigenid_gpu_ctx* c,
            "small batched");
   c->launches += 1;
   c->solves += count * (n + 1);
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
+                                  size_t n, size_t i,
+                                  const eigenid_gpu_config* cfg, double* out,
+                                  double* out_raw, eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  if (i >= n) {
+    set_err(err, EIGENID_E_INDEX, (long long)i, 0.0, 0, "component index out of range");
+    return EIGENID_E_INDEX;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(c->bMu.ensure(sizeof(double) * n * (n - 1)), "alloc mu");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * n), "alloc out");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
+                           cudaMemcpyHostToDevice, c->stream), "H2D A");
+  eigenid_gpu_config scfg{64, 0.0, 0};
+  st = run_large(c, c->bA.as<double>(), (int)n, 0, (int)n, &scfg, nullptr,
+                 c->bLam.as<double>(), c->bMu.as<double>(), false, err);
+  if (st) return st;
+  int launches = 0;
+  // check_nondegenerate for eigenvalue i (identity.cpp:137-139, :281)
+  EID_CUDA(launch_component(c->bLam.as<double>(), c->bMu.as<double>(), (int)n,
+                            (int)i, batch_of(cfg, (int)n), cfg->degeneracy_tol,
+                            cfg->log_domain, c->bOut.as<double>(), c->dstatus,
+                            c->stream, &launches), "gap check");
+  EID_CUDA(launch_vector(c->bLam.as<double>(), c->bMu.as<double>(), (int)n,
+                         (int)i, batch_of(cfg, (int)n), c->bOut.as<double>(),
+                         c->dstatus, c->stream, &launches), "vector");
+  c->launches += launches;
+  std::vector<double> raw(n);
+  EID_CUDA(cudaMemcpyAsync(raw.data(), c->bOut.p, sizeof(double) * n,
+                           cudaMemcpyDeviceToHost, c->stream), "D2H");
+  bool degenerate = false;
+  st = finish(c, err, &degenerate);
+  c->solves += (st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1;
+  if (st) return st;
+  for (size_t t = 0; t < n; ++t) {
+    out[t] = raw[t] < 0.0 ? 0.0 : (1.0 < raw[t] ? 1.0 : raw[t]);
+    if (out_raw) out_raw[t] = raw[t];
+  }
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* c, const double* a,
+                                    size_t n, size_t i, size_t j,
+                                    const double* lambda, const double* mu_j,
+                                    const eigenid_gpu_config* cfg,
+                                    double* value, double* raw, int* method,
+                                    eigenid_gpu_err* err) {
+  if (n < 2) return check_n(n, err);
+  int st = check_cfg(cfg, err);
+  if (st) return st;
+  if (i >= n || j >= n) {  // check_component_indices, identity.cpp:28-36
+    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, "component index out of range");
+    return EIGENID_E_INDEX;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(c->bMu.ensure(sizeof(double) * n), "alloc mu");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * 4), "alloc out");
+  size_t solves = 0;
+  if (lambda && mu_j) {
+    EID_CUDA(cudaMemcpyAsync(c->bLam.p, lambda, sizeof(double) * n,
+                             cudaMemcpyHostToDevice, c->stream), "H2D lambda");
+    EID_CUDA(cudaMemcpyAsync(c->bMu.p, mu_j, sizeof(double) * (n - 1),
+                             cudaMemcpyHostToDevice, c->stream), "H2D mu");
+  } else {
+    if (n > (size_t)kLargeMax) return check_n(n, err);
+    EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
+    EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
+                             cudaMemcpyHostToDevice, c->stream), "H2D A");
+    eigenid_gpu_config scfg{64, 0.0, 0};
+    st = run_large(c, c->bA.as<double>(), (int)n, (int)j, (int)j + 1, &scfg,
+                   nullptr, c->bLam.as<double>(), c->bMu.as<double>(), false,
+                   err);
+    if (st) return st;
+    solves = 2;
+  }
+  int launches = 0;
+  EID_CUDA(launch_component(c->bLam.as<double>(), c->bMu.as<double>(), (int)n,
+                            (int)i, batch_of(cfg, (int)n), cfg->degeneracy_tol,
+                            cfg->log_domain, c->bOut.as<double>(), c->dstatus,
+                            c->stream, &launches), "component");
+  c->launches += launches;
+  double h[3];
+  EID_CUDA(cudaMemcpyAsync(h, c->bOut.p, sizeof(double) * 3,
+                           cudaMemcpyDeviceToHost, c->stream), "D2H");
+  st = finish(c, err, nullptr);
+  c->solves += solves;
+  if (st) return st;
+  *value = h[0];
+  if (raw) *raw = h[1];
+  if (method) *method = (int)h[2];
   return EIGENID_OK;
 }
 

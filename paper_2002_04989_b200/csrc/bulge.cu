@@ -239,6 +239,7 @@ bulge_chase_kernel(Stage2Args a) {
         BPH(0);
         if (haven) {
           wait_prev(prog, warp, st, k + 2);
+          BPH(6);
           load_c(ncrow, AB, Rn, Ln, Rk, Lk);
           prefetch_d(sDb[buf ^ 1], AB, Rn, Ln);
         }

@@ -276,6 +276,76 @@ __global__ void c5_mu_kernel(uint64_t seed, const double* __restrict__ lam,
   }
 }
 
+// evaluate() for one (i, j) with raw value and method (identity.cpp:185-238):
+// checked_min_gap for i (identity.cpp:189), batched product, log-domain
+// retry, clamp.  out3 = {value, raw, method}.
+__global__ void component_kernel(const double* __restrict__ lam,
+                                 const double* __restrict__ mu, int n, int i,
+                                 int batch, double tol, int log_domain,
+                                 double* out3, DevStatus* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double min_gap = 1e308;
+  for (int k = 0; k < n; ++k)
+    if (k != i) min_gap = fmin(min_gap, fabs(lam[i] - lam[k]));
+  if (min_gap <= tol * (lam[n - 1] - lam[0])) {
+    set_status(status, 2, i, min_gap, -1, 1);
+    return;
+  }
+  double raw;
+  int method = 1;
+  if (log_domain) {
+    const int rc = identity_log_domain(lam, mu, n, i, &raw);
+    if (rc) { set_status(status, rc, i, 0.0); return; }
+    method = 3;
+  } else {
+    raw = identity_batched(lam, mu, n, i, batch);
+    if (!isfinite(raw)) {
+      const int rc = identity_log_domain(lam, mu, n, i, &raw);
+      if (rc) { set_status(status, rc, i, 0.0); return; }
+      method = 3;
+    }
+  }
+  out3[0] = clamp01(raw);
+  out3[1] = raw;
+  out3[2] = method;
+}
+
+// raw |v_ij|^2 of one eigenvector i for every row j (vector_magnitudes).
+__global__ void vector_kernel(const double* __restrict__ lam,
+                              const double* __restrict__ mu, int n, int i,
+                              int batch, double* __restrict__ raw_out,
+                              DevStatus* status) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += gridDim.x * blockDim.x) {
+    const double* mj = mu + (long long)j * (n - 1);
+    double raw = identity_batched(lam, mj, n, i, batch);
+    if (!isfinite(raw)) {
+      const int rc = identity_log_domain(lam, mj, n, i, &raw);
+      if (rc) set_status(status, rc, i, 0.0, j);
+    }
+    raw_out[j] = raw;
+  }
+}
+
+cudaError_t launch_component(const double* dlam, const double* dmu, int n,
+                             int i, int batch, double tol, int log_domain,
+                             double* dout3, DevStatus* dstatus, cudaStream_t st,
+                             int* launches) {
+  component_kernel<<<1, 32, 0, st>>>(dlam, dmu, n, i, batch, tol, log_domain,
+                                     dout3, dstatus);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
+                          int batch, double* draw, DevStatus* dstatus,
+                          cudaStream_t st, int* launches) {
+  vector_kernel<<<(n + 127) / 128, 128, 0, st>>>(dlam, dmu, n, i, batch, draw,
+                                                 dstatus);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // ---- launchers ----------------------------------------------------------
 
 int identity_nb(int n, int batch) { return (n - 1 + batch - 1) / batch; }

@@ -104,6 +104,39 @@ class SymmetricMatrix:
         return float(np.trace(self.array()))
 
 
+def random_symmetric(seed: int, n: int, dist: str = "gaussian") -> np.ndarray:
+    """random_symmetric (matrix_io.cpp:171-181): the reference's seeded
+    generator (mt19937_64, Box-Muller / uniform(-1,1), build(kSymmetrize)),
+    bit-identical; host code in the C-ABI library."""
+    out = np.empty((n, n), np.float64)
+    _native.load().eigenid_random_symmetric(seed, n, 1 if dist == "uniform" else 0,
+                                            _native.dptr(out))
+    return out
+
+
+def seeded_draws(seed: int, count: int, dist: str = "gaussian") -> np.ndarray:
+    """The reference's raw SeededDraws stream (matrix_io.cpp:44-65)."""
+    out = np.empty(count, np.float64)
+    _native.load().eigenid_seeded_draws(seed, count, 1 if dist == "uniform" else 0,
+                                        _native.dptr(out))
+    return out
+
+
+def c5_lambda(seed: int, n: int) -> np.ndarray:
+    """C5 synthetic spectrum: n uniform(-1,1) draws, sorted,
+    ties re-drawn from the same stream (strictly increasing)."""
+    draws = seeded_draws(seed, 2 * n, "uniform")
+    lam = np.sort(draws[:n])
+    extra = iter(draws[n:])
+    while True:
+        tie = np.nonzero(lam[1:] == lam[:-1])[0]
+        if tie.size == 0:
+            return lam
+        for k in tie:
+            lam[k + 1] = next(extra)
+        lam = np.sort(lam)
+
+
 def _as_matrix(a) -> tuple[int, np.ndarray]:
     if isinstance(a, SymmetricMatrix):
         return a.n(), np.ascontiguousarray(a.entries())
@@ -260,6 +293,54 @@ class IdentityEngine:
         self._count(b)
         _native.check(st, err)
         return out
+
+    def vector_magnitudes(self, a, i: int, return_raw: bool = False):
+        """|v_ij|^2 for j = 0..n-1 (identity.cpp:276-292): n+1 solves."""
+        n, e = _as_matrix(a)
+        out = np.empty(n, np.float64)
+        raw = np.empty(n, np.float64)
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        b = self._before()
+        st = self._dev.lib.eigenid_gpu_vector_magnitudes(
+            self._dev.ctx, _native.dptr(e), n, i, C.byref(cfg), _native.dptr(out),
+            _native.dptr(raw), C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        return (out, raw) if return_raw else out
+
+    def component_magnitude(self, a, i: int, j: int, cached_lambda=None,
+                            cached_mu=None):
+        """(value, raw_value, method) of |v_ij|^2 (identity.cpp:240-251);
+        cached spectra skip the two solves (SPEC D6)."""
+        if isinstance(a, SymmetricMatrix) or a is not None:
+            n, e = _as_matrix(a)
+        else:
+            n, e = len(cached_lambda), np.zeros(1)
+        lam = None if cached_lambda is None else np.ascontiguousarray(cached_lambda, np.float64)
+        mu = None if cached_mu is None else np.ascontiguousarray(cached_mu, np.float64)
+        v, r, m = C.c_double(), C.c_double(), C.c_int()
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        b = self._before()
+        st = self._dev.lib.eigenid_gpu_component_magnitude(
+            self._dev.ctx, _native.dptr(e), n, i, j,
+            _native.dptr(lam) if lam is not None else None,
+            _native.dptr(mu) if mu is not None else None, C.byref(cfg),
+            C.byref(v), C.byref(r), C.byref(m), C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        return v.value, r.value, m.value
+
+    def log_domain_magnitude(self, a, i: int, j: int, cached_lambda=None,
+                             cached_mu=None):
+        """log_domain_magnitude (identity.cpp:253-274)."""
+        saved = self._cfg.evaluation
+        self._cfg.evaluation = "log-domain"
+        try:
+            return self.component_magnitude(a, i, j, cached_lambda, cached_mu)
+        finally:
+            self._cfg.evaluation = saved
 
     def minor_spectra(self, a, j0: int = 0, j1: int | None = None):
         """lambda(A) and the ascending spectra of minors j0..j1-1."""

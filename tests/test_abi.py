@@ -13,7 +13,7 @@ LIB = os.path.join(ROOT, "paper_2002_04989_b200", "libeigenid_b200.so")
 
 def declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(eigenid_gpu_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(eigenid_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_entry_points():

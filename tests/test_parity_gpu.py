@@ -255,3 +255,50 @@ def test_cpp_host_layer():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
+
+
+# ------------------------------------------------------------- §8 f2 / f3
+def test_vector_magnitudes(oracle):
+    """vector_magnitudes (identity.cpp:276-292): one eigenvector's
+    magnitudes, n+1 solves, unit norm."""
+    from paper_2002_04989_b200 import IdentityEngine
+    eng = IdentityEngine()
+    for n, i in ((30, 0), (30, 17), (90, 45)):
+        a = oracle.random_symmetric(2, n)
+        eng.reset_solve_count()
+        v = eng.vector_magnitudes(a, i)
+        assert eng.eigenvalue_solve_count() == n + 1
+        want = oracle.all_magnitudes(a)[:, i]
+        assert mixed_ok(v, want)
+        assert abs(v.sum() - 1.0) <= 1e-10
+
+
+def test_component_magnitude_cached_is_bit_exact(oracle):
+    from paper_2002_04989_b200 import IdentityEngine
+    eng = IdentityEngine()
+    a = oracle.random_symmetric(9, 50)
+    _, lam, mu = oracle.all_magnitudes(a, return_spectra=True)
+    eng.reset_solve_count()
+    for i, j in ((25, 7), (0, 0), (49, 49)):
+        v, raw, meth = eng.component_magnitude(a, i, j, lam, mu[j])
+        ov, oraw, ometh = oracle.evaluate(lam, mu[j], i)
+        assert (v, raw, meth) == (ov, oraw, ometh)
+    assert eng.eigenvalue_solve_count() == 0      # cached spectra: no solves
+    v, raw, _ = eng.component_magnitude(a, 25, 7)
+    assert eng.eigenvalue_solve_count() == 2      # A and M_7
+    assert mixed_ok(np.array([v]), np.array([oracle.all_magnitudes(a)[7, 25]]))
+    lv, _, lmeth = eng.log_domain_magnitude(a, 25, 7, lam, mu[7])
+    assert lmeth == 3 and abs(lv - oracle.evaluate(lam, mu[7], 25)[0]) <= 1e-12 * lv
+    hv, _, _ = eng.component_magnitude(np.array([[2.0, 1.0], [1.0, 2.0]]), 0, 0)
+    assert abs(hv - 0.5) <= 1e-12
+
+
+def test_component_magnitude_errors(oracle):
+    import paper_2002_04989_b200 as eid
+    eng = eid.IdentityEngine()
+    with pytest.raises(eid.IndexOutOfRange):
+        eng.component_magnitude(oracle.random_symmetric(1, 5), 5, 0)
+    with pytest.raises(eid.DegenerateEigenvalue):
+        eng.component_magnitude(np.eye(5), 0, 0)
+    with pytest.raises(eid.DegenerateEigenvalue):
+        eng.vector_magnitudes(np.eye(5), 0)

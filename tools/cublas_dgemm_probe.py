@@ -30,3 +30,5 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record(); c.baddbmm_(a, b); e1.record(); e1.synchronize()
 t = e0.elapsed_time(e1) / 1e3
 print(f"batched 148 x (4095^2 += 4095x64 . 64x4095): {2*148*4095*4095*64/t/1e12:.2f} TFLOP/s")
+for (m, n, k) in [(4095, 4095, 128), (4095, 64, 4095), (4095, 4095, 256), (4095, 128, 4095)]:
+    print(f"dgemm m={m} n={n} k={k}: {bench(m, n, k):.2f} TFLOP/s", flush=True)

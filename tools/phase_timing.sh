@@ -24,8 +24,8 @@ print('stage 1 (CTA 0):')
 for i in range(8): print(f'  {names[i]:10s} {buf[i]/1.965e9*1e3:9.2f} ms  {100*buf[i]/max(tot,1):5.1f}%')
 b2 = (ctypes.c_ulonglong * 8)()
 lib.eigenid_debug_bulge_cycles(b2)
-names = ['loop/sweep', 'prefetch issue', 'right-apply+hh', 'left-apply+C store', 'wait D', 'two-sided+store']
-tot = sum(b2[i] for i in range(6))
+names = ['loop/sweep', 'prefetch issue', 'right-apply+hh', 'left-apply+C store', 'wait D', 'two-sided+store', 'wait prev sweep']
+tot = sum(b2[i] for i in range(7))
 print('stage 2 (warp 0):')
-for i in range(6): print(f'  {names[i]:20s} {b2[i]/1.965e9*1e3:9.2f} ms  {100*b2[i]/max(tot,1):5.1f}%')
+for i in range(7): print(f'  {names[i]:20s} {b2[i]/1.965e9*1e3:9.2f} ms  {100*b2[i]/max(tot,1):5.1f}%')
 PY
