@@ -86,20 +86,26 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
   const int per = (m + a.split - 1) / a.split;
   const int k0 = part * per, k1 = min(m, k0 + per);
   for (int k = k0 + threadIdx.x; k < k1; k += kBisNT) {
-    double lo = glo, hi = ghi;
+    double res = 0.0;
+    bool done = false;
     if (a.lam) {
-      const double l0 = a.lam[k] - delta, l1 = a.lam[k + 1] + delta;
-      if (sturm_count(sd, se2, m, l0 * sc) <= k &&
-          sturm_count(sd, se2, m, l1 * sc) > k) {
-        lo = fmax(l0, glo);
-        hi = fmin(l1, ghi);
-        if (!(lo < hi)) {
-          lo = glo;
-          hi = ghi;
+      // interlacing bracket, verified by the Sturm counts at both ends; the
+      // end evaluations seed the secant iteration
+      const double l0 = fmax(a.lam[k] - delta, glo), l1 = fmin(a.lam[k + 1] + delta, ghi);
+      double p0, p1;
+      int e0, e1;
+      const int c0 = sturm_det(sd, se2, m, l0 * sc, &p0, &e0);
+      if (c0 <= k && l0 < l1) {
+        const int c1 = sturm_det(sd, se2, m, l1 * sc, &p1, &e1);
+        if (c1 > k) {
+          res = bisect_from(sd, se2, m, k, l0 * sc, l1 * sc, atol, c0, p0, e0,
+                            c1, p1, e1);
+          done = true;
         }
       }
     }
-    out[k] = bisect_one(sd, se2, m, k, lo * sc, hi * sc, atol) / sc;
+    if (!done) res = bisect_one(sd, se2, m, k, glo * sc, ghi * sc, atol);
+    out[k] = res / sc;
   }
   if (a.split > 1) return;  // cross-CTA order is checked by sort_fix_kernel
   __syncthreads();

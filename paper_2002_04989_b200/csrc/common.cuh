@@ -53,6 +53,64 @@ __device__ __forceinline__ void set_status(DevStatus* st, int code,
   }
 }
 
+// Power-of-two scale 2^-e with 2^e >= tn (exact rescaling of T).
+__device__ __forceinline__ double pow2_scale(double tn) {
+  if (!(tn > 0.0)) return 1.0;
+  return scalbn(1.0, -(ilogb(tn) + 1));
+}
+
+// Sturm count plus the determinant det(T - x) = p * 2^e of the same
+// division-free recurrence (sign(det) = (-1)^count); used for the secant
+// (Illinois) acceleration of bisection.
+__device__ __forceinline__ bool is_zero_bits(double v) {
+  // +-0.0 test on the integer pipe (keeps the FP64 pipe for the recurrence)
+  return ((__double2hiint(v) & 0x7fffffff) | __double2loint(v)) == 0;
+}
+
+__device__ __forceinline__ int biased_exp(double v) {
+  return (__double2hiint(v) >> 20) & 0x7ff;
+}
+
+__device__ __forceinline__ int sturm_det(const double* __restrict__ d,
+                                         const double* __restrict__ e2, int m,
+                                         double x, double* pdet, int* edet) {
+  double p0 = 1.0, p1 = d[0] - x;
+  if (is_zero_bits(p1)) p1 = -0x1p-900;
+  int cnt = __double2hiint(p1) < 0;
+  int ex = 0;
+  int k = 1;
+  for (; k + 4 <= m; k += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double p2 = fma(d[k + u] - x, p1, -e2[k + u - 1] * p0);
+      if (is_zero_bits(p2)) p2 = -p1 * 0x1p-900;
+      cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+      p0 = p1;
+      p1 = p2;
+    }
+    // renormalise by a power of two when the larger exponent leaves
+    // [2^-256, 2^256] (integer test on the exponent fields)
+    const int eb = max(biased_exp(p0), biased_exp(p1));
+    if (eb > 1023 + 256 || eb < 1023 - 256) {
+      const int sh = eb - 1023;
+      const double f = __hiloint2double((1023 - sh) << 20, 0);
+      p0 *= f;
+      p1 *= f;
+      ex += sh;
+    }
+  }
+  for (; k < m; ++k) {
+    double p2 = fma(d[k] - x, p1, -e2[k - 1] * p0);
+    if (is_zero_bits(p2)) p2 = -p1 * 0x1p-900;
+    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+    p0 = p1;
+    p1 = p2;
+  }
+  *pdet = p1;
+  *edet = ex;
+  return cnt;
+}
+
 // Sturm count: number of eigenvalues of the symmetric tridiagonal (d, e2)
 // strictly below x, division-free form p_k = (d_k - x) p_{k-1} - e2_{k-1}
 // p_{k-2}, counting sign changes (Sturm sequence of leading minors).  The
@@ -64,81 +122,9 @@ __device__ __forceinline__ void set_status(DevStatus* st, int code,
 __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
                                            const double* __restrict__ e2,
                                            int m, double x) {
-  double p0 = 1.0, p1 = d[0] - x;
-  if (p1 == 0.0) p1 = -0x1p-900;
-  int cnt = __double2hiint(p1) < 0;
-  int k = 1;
-  for (; k + 4 <= m; k += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double p2 = fma(d[k + u] - x, p1, -e2[k + u - 1] * p0);
-      if (p2 == 0.0) p2 = -p1 * 0x1p-900;
-      cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
-      p0 = p1;
-      p1 = p2;
-    }
-    const double mx = fmax(fabs(p0), fabs(p1));
-    if (mx > 0x1p256 || mx < 0x1p-256) {
-      const double f = scalbn(1.0, -ilogb(mx));
-      p0 *= f;
-      p1 *= f;
-    }
-  }
-  for (; k < m; ++k) {
-    double p2 = fma(d[k] - x, p1, -e2[k - 1] * p0);
-    if (p2 == 0.0) p2 = -p1 * 0x1p-900;
-    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
-    p0 = p1;
-    p1 = p2;
-  }
-  return cnt;
-}
-
-// Power-of-two scale 2^-e with 2^e >= tn (exact rescaling of T).
-__device__ __forceinline__ double pow2_scale(double tn) {
-  if (!(tn > 0.0)) return 1.0;
-  return scalbn(1.0, -(ilogb(tn) + 1));
-}
-
-// Sturm count plus the determinant det(T - x) = p * 2^e of the same
-// division-free recurrence (sign(det) = (-1)^count); used for the secant
-// (Illinois) acceleration of bisection.
-__device__ __forceinline__ int sturm_det(const double* __restrict__ d,
-                                         const double* __restrict__ e2, int m,
-                                         double x, double* pdet, int* edet) {
-  double p0 = 1.0, p1 = d[0] - x;
-  if (p1 == 0.0) p1 = -0x1p-900;
-  int cnt = __double2hiint(p1) < 0;
-  int ex = 0;
-  int k = 1;
-  for (; k + 4 <= m; k += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double p2 = fma(d[k + u] - x, p1, -e2[k + u - 1] * p0);
-      if (p2 == 0.0) p2 = -p1 * 0x1p-900;
-      cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
-      p0 = p1;
-      p1 = p2;
-    }
-    const double mx = fmax(fabs(p0), fabs(p1));
-    if (mx > 0x1p256 || mx < 0x1p-256) {
-      const int sh = ilogb(mx);
-      const double f = scalbn(1.0, -sh);
-      p0 *= f;
-      p1 *= f;
-      ex += sh;
-    }
-  }
-  for (; k < m; ++k) {
-    double p2 = fma(d[k] - x, p1, -e2[k - 1] * p0);
-    if (p2 == 0.0) p2 = -p1 * 0x1p-900;
-    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
-    p0 = p1;
-    p1 = p2;
-  }
-  *pdet = p1;
-  *edet = ex;
-  return cnt;
+  double pd;
+  int ed;
+  return sturm_det(d, e2, m, x, &pd, &ed);
 }
 
 // Eigenvalue k (0-based, ascending) of the scaled (d, e2) inside [lo, hi)
@@ -149,14 +135,12 @@ __device__ __forceinline__ int sturm_det(const double* __restrict__ d,
 // the same eigenvalue bisection would find.  Stops at
 // hi - lo <= max(atol, 2 eps max(|lo|,|hi|)) — the accuracy the
 // Householder reduction's backward error (~eps ||T||) supports.
-__device__ __forceinline__ double bisect_one(const double* __restrict__ d,
-                                             const double* __restrict__ e2,
-                                             int m, int k, double lo, double hi,
-                                             double atol) {
-  double plo, phi;
-  int elo, ehi;
-  int clo = sturm_det(d, e2, m, lo, &plo, &elo);
-  int chi = sturm_det(d, e2, m, hi, &phi, &ehi);
+__device__ __forceinline__ double bisect_from(const double* __restrict__ d,
+                                              const double* __restrict__ e2,
+                                              int m, int k, double lo,
+                                              double hi, double atol, int clo,
+                                              double plo, int elo, int chi,
+                                              double phi, int ehi) {
   int side = 0;
   for (int it = 0; it < 300; ++it) {
     const double w = hi - lo;
@@ -197,6 +181,17 @@ __device__ __forceinline__ double bisect_one(const double* __restrict__ d,
     }
   }
   return lo + 0.5 * (hi - lo);
+}
+
+__device__ __forceinline__ double bisect_one(const double* __restrict__ d,
+                                             const double* __restrict__ e2,
+                                             int m, int k, double lo, double hi,
+                                             double atol) {
+  double plo, phi;
+  int elo, ehi;
+  const int clo = sturm_det(d, e2, m, lo, &plo, &elo);
+  const int chi = sturm_det(d, e2, m, hi, &phi, &ehi);
+  return bisect_from(d, e2, m, k, lo, hi, atol, clo, plo, elo, chi, phi, ehi);
 }
 
 // One |v_ij|^2 exactly as evaluate() computes it (identity.cpp:185-238):
