@@ -48,14 +48,18 @@ __global__ void den_table_kernel(const double* __restrict__ lam, int n,
   rcp[t] = __drcp_rn(dn);
 }
 
+// exponent field within [2^-959, 2^960]: an integer test that keeps the
+// FP64 pipe free for the products
+__device__ __forceinline__ bool mid_range(double v) {
+  const unsigned e = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
+  return e - 64u < 1920u;  // 64 <= e < 1984
+}
+
 __device__ __forceinline__ double div_rn_fast(double a, double b, double r) {
   const double q = __dmul_rn(a, r);
   const double res = __fma_rn(-q, b, a);
   const double q2 = __fma_rn(res, r, q);
-  const double aq = fabs(q2);
-  if (!(aq >= 1e-290 && aq <= 1e290) || !(fabs(a) >= 1e-290) ||
-      !(fabs(b) >= 1e-290 && fabs(b) <= 1e290))
-    return __ddiv_rn(a, b);
+  if (!(mid_range(q2) && mid_range(a) && mid_range(b))) return __ddiv_rn(a, b);
   return q2;
 }
 
@@ -97,6 +101,7 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
                 double* __restrict__ out, unsigned long long* flag_count,
                 long long* flags, long long flag_cap) {
   __shared__ double smu[2][kIdTJ * (kIdCH + 1)];
+  __shared__ double sden[2][2 * kIdTI];  // den, rcp of the batch ending in a chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = blockIdx.x * kIdTI, jt = blockIdx.y * kIdTJ;
   const long long ldmu = n - 1;
@@ -119,13 +124,36 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
 
   const int total = n - 1;  // number of factor pairs
   const int nchunks = (total + kIdCH - 1) / kIdCH;
+  // With batch >= kIdCH at most one batch ends inside a chunk; its den/rcp
+  // rows for this CTA's 256 i are staged with the chunk (cp.async) instead of
+  // being loaded at the batch end.
+  const bool staged_den = batch >= kIdCH;
+  auto stage_den = [&](int c, int buf) {
+    if (!staged_den) return;
+    const int s0 = c * kIdCH, s1 = min(s0 + kIdCH, total);
+    // the batch whose last pair lies in [s0, s1), if any
+    int bend;
+    if (s1 == total) {
+      bend = (total - 1) / batch;
+    } else {
+      bend = s1 / batch - 1;
+      if (bend < 0 || (bend + 1) * batch - 1 < s0) return;
+    }
+    for (int t = threadIdx.x; t < kIdTI; t += blockDim.x) {
+      const long long g = (long long)min(i0 + t, n - 1) * nb + bend;
+      cp_async8(&sden[buf][t], den + g);
+      cp_async8(&sden[buf][kIdTI + t], rcp + g);
+    }
+  };
   stage_mu(smu[0], mu, ldmu, rows, jt, n, 0);
+  stage_den(0, 0);
   cp_async_commit();
   int batch_end = min(batch, total);
   int b = 0;
   for (int c = 0; c < nchunks; ++c) {
     if (c + 1 < nchunks) {
       stage_mu(smu[(c + 1) & 1], mu, ldmu, rows, jt, n, (c + 1) * kIdCH);
+      stage_den(c + 1, (c + 1) & 1);
       cp_async_commit();
       cp_async_wait_1();
     } else {
@@ -150,8 +178,15 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
       if (s == batch_end) {
 #pragma unroll
         for (int q = 0; q < kIdQI; ++q) {
-          const long long t = (long long)min(ii[q], n - 1) * nb + b;
-          const double dq = den[t], rq = rcp[t];
+          double dq, rq;
+          if (staged_den) {
+            dq = sden[c & 1][lane + 32 * q];
+            rq = sden[c & 1][kIdTI + lane + 32 * q];
+          } else {
+            const long long t = (long long)min(ii[q], n - 1) * nb + b;
+            dq = den[t];
+            rq = rcp[t];
+          }
 #pragma unroll
           for (int p = 0; p < kIdPJ; ++p) {
             acc[q][p] = __dmul_rn(acc[q][p], div_rn_fast(num[q][p], dq, rq));
