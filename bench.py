@@ -470,9 +470,20 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
     if wl in ("C3", "C4"):
         t1 = statistics.mean(stage1_ms) / 1e3
         achieved = f_tri(n, rows) / t1 / 1e12
+        # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
+        # --set full capture of a 296-solve wave (profiles/
+        # r01_band_4096_2cta_raw_summary.csv: 4.477 TB read + 1.015 TB
+        # written), scaled to this launch's solve count
+        traffic = (4.477065e12 + 1.014975e12) / 296 * (rows + 1) if n == 4096 else None
         roof = {"bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
                 "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": None,
+                "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": traffic,
+                "traffic_note": ("ncu dram__bytes_read+write per solve x solves; "
+                                 "HBM rate = traffic / launch time"),
+                "hbm_GBps": (traffic / t1 / 1e9) if traffic else None,
+                "ceiling_note": ("cuBLAS DGEMM on the stage-1 update shapes reaches 18.9 "
+                                 "(n=32 SYMM) / 20.3 (k=64 SYR2K) TFLOP/s on this B200 "
+                                 "(profiles/r01_cublas_dgemm_ceilings.txt)"),
                 "peak_source": P_FP64_SOURCE,
                 "algorithmic": "F_tri = (4/3)[n^3 + rows (n-1)^3] flops per launch",
                 "launch_ms": t1 * 1e3, "share_of_step": t1 * 1e3 / ms_step}
