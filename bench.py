@@ -141,11 +141,18 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = "nccl"
 
     def init(self, backend: str):
+        self.backend = backend
         if self.world > 1:
+            import torch
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            # one rank per GPU; with --dist-backend gloo several ranks may
+            # share a GPU to exercise the multi-rank flow (host collectives)
+            ndev = max(torch.cuda.device_count(), 1)
+            self.local = self.local % ndev
             dist.init_process_group(backend=backend)
             self.pg = dist
 
@@ -157,7 +164,8 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if self.backend == "nccl" else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -354,8 +362,12 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
             eng.all_magnitudes_device(a_dev.data_ptr(), n, j0, j1, out_dev.data_ptr(),
                                       lam_dev.data_ptr(), mu_dev.data_ptr())
             if world > 1:
-                with torch.cuda.stream(stream):
-                    full = gather_rows(out_dev, n, world, dist.pg)
+                if dist.backend == "nccl":
+                    with torch.cuda.stream(stream):
+                        full = gather_rows(out_dev, n, world, dist.pg)
+                else:  # host collective (gloo): the rows travel through the CPU
+                    stream.synchronize()
+                    full = gather_rows(out_dev.cpu(), n, world, dist.pg)
         flops = f_tri(n, rows) + f_id(n, rows)
     elif wl == "C2":
         count = 4096
@@ -442,6 +454,8 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
                 step()
                 with torch.cuda.stream(stream):
                     out_pin.copy_(full, non_blocking=True)
+            if dist.backend != "nccl":
+                torch.cuda.synchronize()
             e1.record(stream)
             e1.synchronize()
             te = dist.max(e0.elapsed_time(e1) / 1e3)
@@ -524,6 +538,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo lets several ranks share one GPU (flow testing only)")
     args = ap.parse_args()
     dist = Dist()
     cfg = config_desc(args.config, dist.world)
@@ -532,7 +548,7 @@ def main():
             return 0
         print(json.dumps(reference_arm(args, cfg)), flush=True)
         return 0
-    dist.init("nccl")
+    dist.init(args.dist_backend)
     try:
         line = our_arm(args, dist, cfg)
     finally:
