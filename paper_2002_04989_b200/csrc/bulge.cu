@@ -1,5 +1,5 @@
 // bulge.cu — K1L stage 2: symmetric band (bandwidth kB) -> tridiagonal by
-// Householder bulge chasing.
+// Householder bulge chasing, one warp per solve.
 //
 // Second half of the replacement for tridiagonalize (eigensolve.cpp:19-69).
 // Sweep st annihilates column st below the subdiagonal with a length-kB
@@ -11,31 +11,26 @@
 // position, so a step touches only C and D (band storage keeps 2kB+1
 // diagonals per column).
 //
-// Parallel layout: a CTA owns one solve at a time; its 16 warps form 8 warp
-// pairs and each pair chases one sweep (pair p takes sweeps p, p+8, ...), so
-// 8 consecutive sweeps are in flight: sweep s may run step k once sweep s-1
-// has finished step k+1 (k+2 before prefetching step k+1), tracked by
-// progress counters in shared memory.  The leading sweep pulls each block
-// from HBM and the 7 following sweeps re-read it from L2.  Inside a pair,
-// lane = row and warp h owns columns [16h, 16h+16) of the 32 x 32 blocks, so
-// every step's row dot products are split across the two warps (combined
-// through shared memory under a 64-thread named barrier), halving the
-// per-step dependent chain.  The blocks of step k+1 are prefetched while step
-// k computes (C into registers, D into a shared-memory double buffer by
-// cp.async).  CTAs pull solves from an atomic work counter.
+// A CTA owns one solve at a time and its 8 warps chase 8 consecutive sweeps
+// concurrently (warp w takes sweeps w, w+8, ...): sweep s may run step k once
+// sweep s-1 has finished step k+1 (k+2 before prefetching step k+1), tracked
+// by per-warp progress counters in shared memory.  The leading sweep pulls
+// each block from HBM and the 7 following sweeps re-read it from L2/L1, so
+// band traffic to HBM drops ~8x versus independent solves per warp.  Within
+// a sweep a step never reads what the previous step wrote, so the blocks of
+// step k+1 are prefetched while step k computes (C into registers, lane =
+// row; the full symmetric D into a shared-memory double buffer by cp.async).
+// CTAs pull solves from an atomic work counter (persistent kernel).
 #include "common.cuh"
 
 namespace eigenid_b200 {
 
 constexpr int kCB = 32;              // bandwidth (must match band.cu kB)
 constexpr int kCLD = 2 * kCB + 1;    // band diagonals stored per column
-constexpr int kPairs = 8;            // sweeps in flight per CTA
-constexpr int kWarpsPerCta = 2 * kPairs;
-constexpr int kHalf = kCB / 2;       // columns per warp
-constexpr int kSLD = kCB + 2;        // even: rows read as double2
+constexpr int kWarpsPerCta = 8;
+constexpr int kSLD = kCB + 1;
 constexpr int kBlk = kCB * kSLD;
-// per pair: sC, sD[2], v, v2, w, w2, x[2][32], scalars
-constexpr int kPairSmem = 3 * kBlk + 4 * kCB + 2 * kCB + 8;
+constexpr int kWarpSmem = 3 * kBlk + 3 * kCB;  // sC, sD[2], v, v2, w
 
 struct Stage2Args {
   double* band;            // per solve: m columns x kCLD
@@ -56,24 +51,20 @@ __device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool ok) 
                "l"(gmem), "r"(ok ? 8 : 0));
 }
 // Branch-free predicated store (the compiler otherwise emits one divergent
-// branch per element of the store loops).
+// branch per element of the 32-iteration store loops).
 __device__ __forceinline__ void st_pred(double* p, double v, bool pred) {
   asm volatile(
       "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}\n" ::"l"(p),
       "d"(v), "r"((int)pred)
       : "memory");
 }
+
 __device__ __forceinline__ void cpa_commit2() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cpa_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-// 64-thread barrier of warp pair p (named barriers 1..8).
-__device__ __forceinline__ void pair_sync(int pair) {
-  asm volatile("bar.sync %0, 64;\n" ::"r"(pair + 1) : "memory");
-}
-
-// Householder from x (lane r holds x_r, r < L), one warp: v (v_0 = 1) -> sv,
-// returns tau, *beta (dlarfg convention).
+// Householder from x (lane r holds x_r, r < L): v (v_0 = 1) -> sv, returns
+// tau, *beta.  dlarfg convention.
 __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
                                                    double* beta) {
   const int lane = threadIdx.x & 31;
@@ -90,255 +81,213 @@ __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
     scal = 1.0 / (alpha - b);
   }
   sv[lane] = (lane == 0) ? 1.0 : ((lane < L) ? x * scal : 0.0);
+  __syncwarp();
   *beta = b;
   return tau;
 }
 
-struct PairSmem {
-  double* sC;     // 32 x kSLD: C rows for the left-apply transposition
-  double* sD[2];  // 32 x kSLD: D block double buffer
-  double* sv;     // previous / current reflector
-  double* sv2;    // new reflector
-  double* sw;     // left-apply column weights
-  double* sw2;    // two-sided w vector
-  double* sx;     // [2][32] partial row sums of the two halves
-  double* sc;     // scalars: tau, tau2
-};
-
-// D <- H D H on the L x L block in sD (both triangles, zero outside L); each
-// warp of the pair updates and stores its 16 columns of the lower triangle.
-__device__ __forceinline__ void two_sided_pair(const PairSmem& S, double* sD,
-                                               const double* sv, double tau,
-                                               int L, double* AB, int R,
-                                               int pair, int h) {
+// D <- H D H on the L x L diagonal block held (both triangles) in sD
+// (filled by cp.async; rows/cols >= L are zero).  Writes the lower triangle
+// back to the band.
+__device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
+                                                double tau, double* sw, int L,
+                                                double* AB, int R) {
   const int lane = threadIdx.x & 31;
-  double drow[kHalf];
-  double pp[2] = {0.0, 0.0};
-  const double2* dr2 = reinterpret_cast<const double2*>(sD + lane * kSLD + kHalf * h);
-  const double2* v2p = reinterpret_cast<const double2*>(sv + kHalf * h);
+  double drow[kCB];
+  double pp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int c = 0; c < kHalf / 2; ++c) {
-    const double2 dd = dr2[c], vv = v2p[c];
-    drow[2 * c] = dd.x;
-    drow[2 * c + 1] = dd.y;
-    pp[0] += dd.x * vv.x;
-    pp[1] += dd.y * vv.y;
+  for (int c = 0; c < kCB; ++c) {
+    drow[c] = sD[lane * kSLD + c];
+    pp[c & 3] += drow[c] * sv[c];
   }
-  S.sx[h * kCB + lane] = pp[0] + pp[1];
-  pair_sync(pair);
-  const double p = tau * (S.sx[lane] + S.sx[kCB + lane]);
+  double p = (pp[0] + pp[1]) + (pp[2] + pp[3]);
+  p *= tau;
   const double vr = sv[lane];
   const double K = 0.5 * tau * warp_sum(p * vr);
   const double w = p - K * vr;
-  if (h == 0) S.sw2[lane] = w;
-  pair_sync(pair);
-  const double2* w2p = reinterpret_cast<const double2*>(S.sw2 + kHalf * h);
+  sw[lane] = w;
+  __syncwarp();
 #pragma unroll
-  for (int c = 0; c < kHalf / 2; ++c) {
-    const double2 ww = w2p[c], vv = v2p[c];
-    drow[2 * c] -= vr * ww.x + w * vv.x;
-    drow[2 * c + 1] -= vr * ww.y + w * vv.y;
-  }
-  // lower triangle back to the band: column cg, rows cg..L-1
+  for (int c = 0; c < kCB; ++c) drow[c] -= vr * sw[c] + w * sv[c];
+  // lower triangle back to the band: column c, rows c..L-1 (coalesced in r)
   double* base = AB + (long long)R * kCLD + lane;
 #pragma unroll
-  for (int c = 0; c < kHalf; ++c) {
-    const int cg = kHalf * h + c;
-    st_pred(base + cg * (kCLD - 1), drow[c], lane >= cg && lane < L);
-  }
+  for (int c = 0; c < kCB; ++c)
+    st_pred(base + c * (kCLD - 1), drow[c], lane >= c && lane < L);
+  __syncwarp();
 }
 
-// cp.async of this warp's 16 columns of the symmetric L x L block at R.
-__device__ __forceinline__ void prefetch_d_half(double* sD, const double* AB,
-                                                int R, int L, int h) {
+__device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
+                                           int L) {
+  // full symmetric L x L block: element (r, c) lives at column min(r,c),
+  // diagonal |r - c| of the band; out-of-range entries are zero-filled
   const int lane = threadIdx.x & 31;
   const double* base = AB + (long long)R * kCLD;
 #pragma unroll
-  for (int c = 0; c < kHalf; ++c) {
-    const int cg = kHalf * h + c;
-    const bool ok = lane < L && cg < L;
-    const int off = (cg <= lane) ? cg * kCLD + (lane - cg) : lane * kCLD + (cg - lane);
-    cpa8(sD + lane * kSLD + cg, ok ? base + off : AB, ok);
+  for (int c = 0; c < kCB; ++c) {
+    const bool ok = lane < L && c < L;
+    // (r, c) -> column min(r,c), diagonal |r-c|
+    const int off = (c <= lane) ? c * kCLD + (lane - c) : lane * kCLD + (c - lane);
+    cpa8(sD + lane * kSLD + c, ok ? base + off : AB, ok);
   }
   cpa_commit2();
 }
 
-// This warp's 16 columns of C = A[R1.., R..] (lane = row).
-__device__ __forceinline__ void load_c_half(double (&cr)[kHalf], const double* AB,
-                                            int R1, int L1, int R, int L, int h) {
+__device__ __forceinline__ void load_c(double (&cr)[kCB], const double* AB,
+                                       int R1, int L1, int R, int L) {
   const int lane = threadIdx.x & 31;
   const double* base = AB + (long long)R * kCLD + (R1 - R) + lane;
 #pragma unroll
-  for (int c = 0; c < kHalf; ++c) {
-    const int cg = kHalf * h + c;
-    cr[c] = (lane < L1 && cg < L) ? base[cg * (kCLD - 1)] : 0.0;
-  }
+  for (int c = 0; c < kCB; ++c)
+    cr[c] = (lane < L1 && c < L) ? base[c * (kCLD - 1)] : 0.0;
 }
+
+#ifdef EIGENID_PHASE_TIMING
+__device__ unsigned long long g_bulge_cycles[8];
+#define BPH(id)                                                         \
+  do {                                                                  \
+    const long long now_ = clock64();                                   \
+    if (lane == 0 && blockIdx.x == 0 && warp == 0)                      \
+      g_bulge_cycles[id] += (unsigned long long)(now_ - t_b_);          \
+    t_b_ = now_;                                                        \
+  } while (0)
+#else
+#define BPH(id) \
+  do {          \
+  } while (0)
+#endif
 
 __device__ __forceinline__ long long spos(int sweep, int step) {
   return (long long)sweep * 65536 + step;
 }
 
-// Blocks until sweep s-1 (owned by pair (p-1) mod 8) has finished step k.
-__device__ __forceinline__ void wait_prev(volatile long long* prog, int pair,
+// Blocks until sweep s-1 (owned by warp (w-1) mod 8) has finished step k.
+__device__ __forceinline__ void wait_prev(volatile long long* prog, int warp,
                                           int s, int k) {
   if (s == 0) return;
-  const int pp = (pair + kPairs - 1) % kPairs;
+  const int pw = (warp + kWarpsPerCta - 1) % kWarpsPerCta;
   const long long need = spos(s - 1, k);
   if ((threadIdx.x & 31) == 0)
-    while (prog[pp] < need) __nanosleep(64);
+    while (prog[pw] < need) __nanosleep(64);
   __syncwarp();
   __threadfence_block();
 }
 
-// Called by both warps of the pair after their stores of step k.
-__device__ __forceinline__ void publish(volatile long long* prog, int pair,
-                                        int h, int s, int k) {
+__device__ __forceinline__ void publish(volatile long long* prog, int warp,
+                                        int s, int k) {
+  __syncwarp();
   __threadfence_block();
-  pair_sync(pair);
-  if (h == 0 && (threadIdx.x & 31) == 0) prog[pair] = spos(s, k);
+  if ((threadIdx.x & 31) == 0) prog[warp] = spos(s, k);
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 1)
 bulge_chase_kernel(Stage2Args a) {
+#ifdef EIGENID_PHASE_TIMING
+  long long t_b_ = clock64();
+#endif
   extern __shared__ double smem[];
-  __shared__ long long prog[kPairs];
+  __shared__ long long prog[kWarpsPerCta];
   __shared__ int s_sidx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pair = warp >> 1, h = warp & 1;
-  PairSmem S;
-  {
-    double* b = smem + pair * kPairSmem;
-    S.sC = b;
-    S.sD[0] = b + kBlk;
-    S.sD[1] = b + 2 * kBlk;
-    S.sv = b + 3 * kBlk;
-    S.sv2 = S.sv + kCB;
-    S.sw = S.sv2 + kCB;
-    S.sw2 = S.sw + kCB;
-    S.sx = S.sw2 + kCB;
-    S.sc = S.sx + 2 * kCB;
-  }
+  double* sC = smem + warp * kWarpSmem;
+  double* sDb[2] = {sC + kBlk, sC + 2 * kBlk};
+  double* sv = sC + 3 * kBlk;
+  double* sv2 = sv + kCB;
+  double* sw = sv2 + kCB;
 
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_sidx = atomicAdd(a.counter, 1);
-    if (threadIdx.x < kPairs) prog[threadIdx.x] = -1;
+    if (threadIdx.x < kWarpsPerCta) prog[threadIdx.x] = -1;
     __syncthreads();
     const int sidx = s_sidx;
     if (sidx >= a.nsolves) break;
     const int m = a.js[sidx] < 0 ? a.n : a.n - 1;
     double* AB = a.band + sidx * a.band_stride;
 
-    for (int st = pair; st + 2 < m; st += kPairs) {
+    for (int st = warp; st + 2 < m; st += kWarpsPerCta) {
       const int R0 = st + 1;
       const int L0 = min(kCB, m - 1 - st);
       int Rk = R0 + kCB;
       bool have = Rk <= m - 1;
       int Lk = have ? min(kCB, m - Rk) : 0;
       // block 0 and the prefetch of step 1 need sweep st-1 past step 2
-      wait_prev(prog, pair, st, 2);
+      wait_prev(prog, warp, st, 2);
       const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
-      prefetch_d_half(S.sD[0], AB, R0, L0, h);
-      double ncrow[kHalf];
+      prefetch_d(sDb[0], AB, R0, L0);
+      double ncrow[kCB];
       if (have) {
-        load_c_half(ncrow, AB, Rk, Lk, R0, L0, h);
-        prefetch_d_half(S.sD[1], AB, Rk, Lk, h);
+        load_c(ncrow, AB, Rk, Lk, R0, L0);
+        prefetch_d(sDb[1], AB, Rk, Lk);
       }
-      if (h == 0) {
-        double beta;
-        const double t0 = warp_householder(x, L0, S.sv, &beta);
-        if (lane < L0) AB[(long long)st * kCLD + 1 + lane] = (lane == 0) ? beta : 0.0;
-        if (lane == 0) S.sc[0] = t0;
-      }
+      double beta;
+      double tau = warp_householder(x, L0, sv, &beta);
+      if (lane < L0) AB[(long long)st * kCLD + 1 + lane] = (lane == 0) ? beta : 0.0;
       if (have) cpa_wait_one(); else cpa_wait_all();
-      pair_sync(pair);  // sv, tau and both halves of D_0 visible
-      double tau = S.sc[0];
-      two_sided_pair(S, S.sD[0], S.sv, tau, L0, AB, R0, pair, h);
-      publish(prog, pair, h, st, 0);
+      __syncwarp();
+      two_sided_store(sDb[0], sv, tau, sw, L0, AB, R0);
+      publish(prog, warp, st, 0);
       int R = R0, L = L0, buf = 1, k = 1;
       while (have) {
         // ---- step k on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]
-        double crow[kHalf];
+        double crow[kCB];
 #pragma unroll
-        for (int c = 0; c < kHalf; ++c) crow[c] = ncrow[c];
+        for (int c = 0; c < kCB; ++c) crow[c] = ncrow[c];
         const int Rn = Rk + kCB;
         const bool haven = Rn <= m - 1;
         const int Ln = haven ? min(kCB, m - Rn) : 0;
+        BPH(0);
         if (haven) {
-          wait_prev(prog, pair, st, k + 2);
-          load_c_half(ncrow, AB, Rn, Ln, Rk, Lk, h);
-          prefetch_d_half(S.sD[buf ^ 1], AB, Rn, Ln, h);
+          wait_prev(prog, warp, st, k + 2);
+          BPH(6);
+          load_c(ncrow, AB, Rn, Ln, Rk, Lk);
+          prefetch_d(sDb[buf ^ 1], AB, Rn, Ln);
         }
+        BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
+        double yy[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < kCB; ++c) yy[c & 3] += crow[c] * sv[c];
+        const double y = tau * ((yy[0] + yy[1]) + (yy[2] + yy[3]));
+#pragma unroll
+        for (int c = 0; c < kCB; ++c) crow[c] -= y * sv[c];
+        // new reflector from C's first column
+        double beta2;
+        const double tau2 = warp_householder(crow[0], Lk, sv2, &beta2);
+        crow[0] = (lane == 0) ? beta2 : 0.0;
+        BPH(2);
+        // left-apply to columns 1..L-1: w_c = sum_r v2_r C[r][c]
+#pragma unroll
+        for (int c = 0; c < kCB; ++c) sC[lane * kSLD + c] = crow[c];
+        __syncwarp();
         {
-          const double2* v2p = reinterpret_cast<const double2*>(S.sv + kHalf * h);
-          double yy[2] = {0.0, 0.0};
+          double ww[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int c = 0; c < kHalf / 2; ++c) {
-            const double2 vv = v2p[c];
-            yy[0] += crow[2 * c] * vv.x;
-            yy[1] += crow[2 * c + 1] * vv.y;
-          }
-          S.sx[h * kCB + lane] = yy[0] + yy[1];
-          pair_sync(pair);
-          const double y = tau * (S.sx[lane] + S.sx[kCB + lane]);
-#pragma unroll
-          for (int c = 0; c < kHalf / 2; ++c) {
-            const double2 vv = v2p[c];
-            crow[2 * c] -= y * vv.x;
-            crow[2 * c + 1] -= y * vv.y;
-          }
+          for (int r = 0; r < kCB; ++r) ww[r & 3] += sv2[r] * sC[r * kSLD + lane];
+          const double w = (ww[0] + ww[1]) + (ww[2] + ww[3]);
+          sw[lane] = (lane >= 1 && lane < L) ? tau2 * w : 0.0;
         }
-        // new reflector from C's first column (owned by warp h = 0)
-        if (h == 0) {
-          double beta2;
-          const double t2 = warp_householder(crow[0], Lk, S.sv2, &beta2);
-          crow[0] = (lane == 0) ? beta2 : 0.0;
-          if (lane == 0) S.sc[1] = t2;
-        }
-        pair_sync(pair);  // v2 and tau2 visible; sx free again
-        const double tau2 = S.sc[1];
-        // left-apply to columns 1..L-1 of this warp's half
+        __syncwarp();
         {
-          double2* cr2 = reinterpret_cast<double2*>(S.sC + lane * kSLD + kHalf * h);
+          const double vr = sv2[lane];
 #pragma unroll
-          for (int c = 0; c < kHalf / 2; ++c) cr2[c] = make_double2(crow[2 * c], crow[2 * c + 1]);
-          __syncwarp();
-          const int cl = lane & (kHalf - 1), rh = lane >> 4;
-          const int cg = kHalf * h + cl;
-          double w = 0.0;
-#pragma unroll
-          for (int r = 0; r < kHalf; ++r) {
-            const int rr = kHalf * rh + r;
-            w += S.sv2[rr] * S.sC[rr * kSLD + cg];
-          }
-          w += __shfl_xor_sync(0xffffffffu, w, 16);
-          if (rh == 0) S.sw[cg] = (cg >= 1 && cg < L) ? tau2 * w : 0.0;
-          __syncwarp();
-          const double vr = S.sv2[lane];
-          const double2* w2p = reinterpret_cast<const double2*>(S.sw + kHalf * h);
-#pragma unroll
-          for (int c = 0; c < kHalf / 2; ++c) {
-            const double2 t = w2p[c];
-            crow[2 * c] -= vr * t.x;
-            crow[2 * c + 1] -= vr * t.y;
-          }
+          for (int c = 1; c < kCB; ++c) crow[c] -= vr * sw[c];
         }
         {
           double* base = AB + (long long)R * kCLD + (Rk - R) + lane;
 #pragma unroll
-          for (int c = 0; c < kHalf; ++c) {
-            const int cg = kHalf * h + c;
-            st_pred(base + cg * (kCLD - 1), crow[c], lane < Lk && cg < L);
-          }
+          for (int c = 0; c < kCB; ++c)
+            st_pred(base + c * (kCLD - 1), crow[c], lane < Lk && c < L);
         }
-        // two-sided on the diagonal block (prefetched into sD[buf])
+        BPH(3);
+        // two-sided on the diagonal block (prefetched into sDb[buf])
         if (haven) cpa_wait_one(); else cpa_wait_all();
-        pair_sync(pair);  // both halves of D_k landed
-        two_sided_pair(S, S.sD[buf], S.sv2, tau2, Lk, AB, Rk, pair, h);
-        if (h == 0) S.sv[lane] = S.sv2[lane];
-        publish(prog, pair, h, st, k);
+        __syncwarp();
+        BPH(4);
+        two_sided_store(sDb[buf], sv2, tau2, sw, Lk, AB, Rk);
+        BPH(5);
+        sv[lane] = sv2[lane];
+        publish(prog, warp, st, k);
         tau = tau2;
         R = Rk;
         L = Lk;
@@ -348,7 +297,7 @@ bulge_chase_kernel(Stage2Args a) {
         buf ^= 1;
         ++k;
       }
-      publish(prog, pair, h, st, 65535);  // sweep done
+      publish(prog, warp, st, 65535);  // sweep done
     }
     __syncthreads();
     double* d = a.d + sidx * a.de_stride;
@@ -365,8 +314,14 @@ bulge_chase_kernel(Stage2Args a) {
   }
 }
 
+#ifdef EIGENID_PHASE_TIMING
+extern "C" void eigenid_debug_bulge_cycles(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_bulge_cycles, sizeof(g_bulge_cycles));
+}
+#endif
+
 cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
-  const size_t smem = sizeof(double) * kPairSmem * kPairs;
+  const size_t smem = sizeof(double) * kWarpSmem * kWarpsPerCta;
   cudaError_t e = cudaFuncSetAttribute(
       bulge_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
