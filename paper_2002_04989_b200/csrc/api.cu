@@ -114,10 +114,14 @@ __global__ void init_status_kernel(DevStatus* st) {
   st[1].aux = -1;
 }
 
-__global__ void solve_list_kernel(int* js, int j0, int count) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= count;
-       t += gridDim.x * blockDim.x)
-    js[t] = t == 0 ? -1 : j0 + t - 1;
+// Solve list of one chunk: local t <-> global g = g0 + t; g = 0 is A itself
+// (-1), g >= 1 is minor j0 + g - 1.
+__global__ void solve_list_kernel(int* js, int j0, int g0, int count) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += gridDim.x * blockDim.x) {
+    const int g = g0 + t;
+    js[t] = g == 0 ? -1 : j0 + g - 1;
+  }
 }
 
 }  // namespace eigenid_b200
@@ -269,8 +273,8 @@ constexpr int kStages = 5;  // stage1, stage2, bisect_A, bisect_minors, identity
 struct StageTimer {
   bool on = false, print = false;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[kStages + 1];
-  int slot[kStages + 1];
+  cudaEvent_t ev[4 * kStages + 1];
+  int slot[4 * kStages + 1];
   int count = 0;
   double* sink = nullptr;  // ctx->stage_ms
   StageTimer(cudaStream_t s, bool enabled, double* out) : st(s), sink(out) {
@@ -280,7 +284,7 @@ struct StageTimer {
     mark(-1);
   }
   void mark(int stage) {
-    if (!on || count > kStages) return;
+    if (!on || count > 4 * kStages) return;
     cudaEventCreate(&ev[count]);
     cudaEventRecord(ev[count], st);
     slot[count++] = stage;
@@ -294,7 +298,7 @@ struct StageTimer {
     for (int t = 1; t < count; ++t) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[t - 1], ev[t]);
-      sink[slot[t]] = ms;
+      sink[slot[t]] += ms;
       if (print) std::fprintf(stderr, "[eigenid] %-14s %10.3f ms\n", names[slot[t]], ms);
     }
     for (int t = 0; t < count; ++t) cudaEventDestroy(ev[t]);
@@ -307,51 +311,81 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
               double* dmu, bool identity, eigenid_gpu_err* err) {
   cudaStream_t st = c->stream;
   const int rows = j1 - j0;
-  const int nsolves = 1 + rows;
+  const int nsolves = 1 + rows;  // global solve g: 0 = A, g >= 1 = minor j0+g-1
   const int kB = stage1_bandwidth();
   const int ldab = stage1_band_ld();
   const int ldw = (n + 7) & ~7;
   const long long ws_stride = (long long)n * ldw + 3LL * n * kB;
-  const int slots = nsolves < kStage1Slots ? nsolves : kStage1Slots;
-  int launches = 0;
-  EID_CUDA(c->bJs.ensure(sizeof(int) * (size_t)nsolves), "alloc js");
-  EID_CUDA(c->bWs.ensure(sizeof(double) * (size_t)slots * ws_stride), "alloc ws");
   const long long band_stride = (long long)n * ldab;
-  EID_CUDA(c->bBand.ensure(sizeof(double) * (size_t)nsolves * band_stride),
-           "alloc band");
-  EID_CUDA(c->bD.ensure(sizeof(double) * (size_t)nsolves * n), "alloc d");
-  EID_CUDA(c->bE2.ensure(sizeof(double) * (size_t)nsolves * n), "alloc e2");
-  EID_CUDA(c->bAe.ensure(sizeof(double) * (size_t)nsolves * n), "alloc ae");
+  // Memory plan: stage-1 workspace slots and the number of solves whose band
+  // and tridiagonal are resident at once, sized to the free device memory
+  // (large n is processed in chunks of solves).
+  size_t free_b = 0, total_b = 0;
+  EID_CUDA(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  const double held = (double)(c->bWs.bytes + c->bBand.bytes + c->bD.bytes +
+                               c->bE2.bytes + c->bAe.bytes);
+  double budget = (double)free_b + held - 4.0e9;
+  // EIGENID_MEM_BUDGET (bytes) caps the plan; the tests use it to force the
+  // chunked schedule at small n.
+  if (const char* mb = std::getenv("EIGENID_MEM_BUDGET")) {
+    const double cap = std::atof(mb);
+    if (cap > 0 && cap < budget) budget = cap;
+  }
+  const double ws_bytes = 8.0 * ws_stride;
+  const double solve_bytes = 8.0 * (band_stride + 3.0 * n);
+  int slots = nsolves < kStage1Slots ? nsolves : kStage1Slots;
+  while (slots > 1 && slots * ws_bytes > 0.7 * budget) slots = (slots + 1) / 2;
+  long long chunk = (long long)((budget - slots * ws_bytes) / solve_bytes);
+  if (chunk > nsolves) chunk = nsolves;
+  if (chunk < slots) chunk = slots;
+  if (chunk < 1) chunk = 1;
+  int launches = 0;
+  EID_CUDA(c->bJs.ensure(sizeof(int) * (size_t)chunk), "alloc js");
+  EID_CUDA(c->bWs.ensure(sizeof(double) * (size_t)slots * ws_stride), "alloc ws");
+  EID_CUDA(c->bBand.ensure(sizeof(double) * (size_t)chunk * band_stride), "alloc band");
+  EID_CUDA(c->bD.ensure(sizeof(double) * (size_t)chunk * n), "alloc d");
+  EID_CUDA(c->bE2.ensure(sizeof(double) * (size_t)chunk * n), "alloc e2");
+  EID_CUDA(c->bAe.ensure(sizeof(double) * (size_t)chunk * n), "alloc ae");
+  EID_CUDA(c->bCounter.ensure(sizeof(int) * 4), "alloc counter");
   int* djs = c->bJs.as<int>();
-  solve_list_kernel<<<(nsolves + 255) / 256, 256, 0, st>>>(djs, j0, rows);
-  ++launches;
 
   StageTimer timer(st, c->profiling, c->stage_ms);
-  Stage1Args s1{dA, n, djs, nsolves, c->bWs.as<double>(), ws_stride, ldw,
-                c->bBand.as<double>(), band_stride};
-  EID_CUDA(launch_stage1(s1, slots, st), "stage1");
-  timer.mark(0);
-  ++launches;
-  EID_CUDA(c->bCounter.ensure(sizeof(int) * 4), "alloc counter");
-  Stage2Args s2{c->bBand.as<double>(), band_stride, djs, nsolves, n,
-                c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(), n,
-                c->bCounter.as<int>()};
-  EID_CUDA(launch_stage2(s2, st), "stage2");
-  ++launches;
-  timer.mark(1);
-  // lambda(A): Gershgorin brackets, split across CTAs
-  BisectArgs ba{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
-                n, djs, nsolves, 0, n, nullptr, dlam, n, (n + 255) / 256};
-  EID_CUDA(launch_bisect(ba, 1, n, st, &launches), "bisect A");
-  timer.mark(2);
-  if (identity) EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol,
-                                           c->dstatus, st, &launches),
-                         "degeneracy");
-  if (rows > 0) {
-    BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
-                  n, djs, nsolves, 1, n, dlam, dmu, n - 1, 1};
-    EID_CUDA(launch_bisect(bm, rows, n - 1, st, &launches), "bisect minors");
-    timer.mark(3);
+  for (long long g0 = 0; g0 < nsolves; g0 += chunk) {
+    const int cnt = (int)((nsolves - g0) < chunk ? (nsolves - g0) : chunk);
+    solve_list_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(djs, j0, (int)g0, cnt);
+    ++launches;
+    Stage1Args s1{dA, n, djs, cnt, c->bWs.as<double>(), ws_stride, ldw,
+                  c->bBand.as<double>(), band_stride};
+    EID_CUDA(launch_stage1(s1, cnt < slots ? cnt : slots, st), "stage1");
+    ++launches;
+    timer.mark(0);
+    Stage2Args s2{c->bBand.as<double>(), band_stride, djs, cnt, n,
+                  c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
+                  n, c->bCounter.as<int>()};
+    EID_CUDA(launch_stage2(s2, st), "stage2");
+    ++launches;
+    timer.mark(1);
+    int first = 0;
+    if (g0 == 0) {
+      // lambda(A): Gershgorin brackets, split across CTAs
+      BisectArgs ba{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
+                    n, djs, cnt, 0, n, nullptr, dlam, n, (n + 255) / 256};
+      EID_CUDA(launch_bisect(ba, 1, n, st, &launches), "bisect A");
+      timer.mark(2);
+      if (identity)
+        EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol, c->dstatus, st,
+                                   &launches),
+                 "degeneracy");
+      first = 1;
+    }
+    if (cnt > first) {
+      // minors of this chunk -> mu rows (g0 + first - 1) ..
+      BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
+                    n, djs, cnt, first, n, dlam,
+                    dmu + (size_t)(g0 + first - 1) * (n - 1), n - 1, 1};
+      EID_CUDA(launch_bisect(bm, cnt - first, n - 1, st, &launches), "bisect minors");
+      timer.mark(3);
+    }
   }
   if (identity && rows > 0) {
     const int batch = batch_of(cfg, n);

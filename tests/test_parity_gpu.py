@@ -164,6 +164,23 @@ def test_determinism_and_shard_invariance(engine, oracle):
         assert np.array_equal(bits(out.cpu().numpy()), bits(g1.reshape(n, n)[j0:j1]))
 
 
+def test_chunked_memory_plan_is_bit_identical(engine, oracle, monkeypatch):
+    """A capped memory budget (EIGENID_MEM_BUDGET) forces fewer stage-1 slots
+    and several chunks of minors; every solve is still computed by the same
+    per-solve kernels, so the result must not change by a single bit."""
+    n = 300
+    a = oracle.random_symmetric(77, n)
+    want = engine.all_magnitudes(a)
+    spectra = engine.minor_spectra(a, 0, n)
+    for budget in ("20000000", "3000000"):
+        monkeypatch.setenv("EIGENID_MEM_BUDGET", budget)
+        got = engine.all_magnitudes(a)
+        assert np.array_equal(bits(got), bits(want))
+        for x, y in zip(engine.minor_spectra(a, 0, n), spectra):
+            assert np.array_equal(bits(x), bits(y))
+    monkeypatch.delenv("EIGENID_MEM_BUDGET")
+
+
 # ------------------------------------------------------------- configs
 def test_c1_n64(engine, oracle, gold):
     a = oracle.random_symmetric(1, 64)

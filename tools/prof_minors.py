@@ -7,11 +7,11 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle.oracle import Oracle  # noqa: E402  (input generation only)
+from paper_2002_04989_b200.engine import random_symmetric  # noqa: E402
 from paper_2002_04989_b200 import IdentityEngine  # noqa: E402
 
 n, rows = int(sys.argv[1]), int(sys.argv[2])
-a = Oracle().random_symmetric(42, n) * np.sqrt(2.0 / n)
+a = random_symmetric(42, n) * np.sqrt(2.0 / n)
 eng = IdentityEngine()
 t = time.time()
 lam, mu = eng.minor_spectra(a, 0, rows)

@@ -9,12 +9,12 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle.oracle import Oracle  # noqa: E402  (input generation only)
+from paper_2002_04989_b200.engine import random_symmetric  # noqa: E402
 from paper_2002_04989_b200 import IdentityEngine  # noqa: E402
 
 n = int(sys.argv[1])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-a = Oracle().random_symmetric(42, n) * np.sqrt(2.0 / n)
+a = random_symmetric(42, n) * np.sqrt(2.0 / n)
 eng = IdentityEngine()
 for r in range(reps):
     t = time.time()
