@@ -25,14 +25,11 @@ constexpr int kB = 32;      // bandwidth / panel width
 constexpr int kNT = 256;    // threads per CTA (8 warps)
 constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
-// Shared-memory layout (doubles).  One CTA (8 warps) per SM; the GEMM
+// Shared-memory layout (doubles).  Two CTAs (8 warps each) per SM; the GEMM
 // region is reused by the panel / Gram phases.
-constexpr int kG2M = 64, kG2N = 32, kG2K = 2 * kB, kG2LD = kG2K + 4;  // 68
-constexpr int kG2_A = kG2M * kG2LD;                 // Aop  64 x 64
-constexpr int kG2_B = kG2N * kG2LD;                 // Bop  32 x 64 (x2)
+constexpr int kG2M = 64, kG2N = 32, kG2K = 2 * kB;  // GEMM2 row block / tile / k
 constexpr int kG1M = 64, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 68;
 constexpr int kMT1 = kG1M / 32;                     // 8-row m-tiles per warp
-constexpr int kMT2 = kG2M / 32, kNT2 = kG2N / 16;   // GEMM2 warp tile
 constexpr int kG1_A = kG1M * kG1LDA;                // pass 1: A chunk 128 x 32
 constexpr int kG1_T = kG1K * kG1TLD;                // pass 2: A chunk 32 x 128
 constexpr int kG1_B = kG1K * kG1LDB;                // VT chunk 32 x 32
@@ -40,12 +37,20 @@ constexpr int kSmallLD = kB + 1;
 constexpr int kSmallMat = kB * kSmallLD;            // T, G/Y, M
 constexpr int kGramPart = 8 * kSmallMat;
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
-constexpr int kGemmSmem =
-    cmax(cmax(kG2_A + 2 * kG2_B, 2 * (kG1_A + kG1_B)),
-         cmax(2 * (kG1_T + kG1_B), kGramPart));
+constexpr int kG1S = 3;                             // GEMM 1 cp.async stages
+constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
+constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
+constexpr int kGemmSmem = cmax(kGramPart, kG2S * kG2St - 3 * kSmallMat);
+// GEMM 1 also owns the G and A scratch matrices that follow the GEMM region
+// (both dead while it runs; T, after them, is not).
+constexpr int kGemm1Smem = kGemmSmem + 2 * kSmallMat;
+// GEMM 2 owns G, A and T as well (all dead while it runs).
+static_assert(kG2S * kG2St <= kGemmSmem + 3 * kSmallMat, "gemm2 smem");
+static_assert(kG1S * (kG1_A + kG1_B) <= kGemm1Smem &&
+                  kG1S * (kG1_T + kG1_B) <= kGemm1Smem, "gemm1 smem");
 constexpr int kRed = 8 + 8 * kB;
 // T, G/Y, A persist across Gram calls; B and R live in the GEMM region
-// (never alive across a gram() or GEMM call).  ~98 KB: two CTAs per SM.
+// (never alive across a gram() or GEMM call).  ~101 KB: two CTAs per SM.
 constexpr int kStage1SmemDoubles = kGemmSmem + 3 * kSmallMat + kRed + 4 * kB;
 static_assert(kGemmSmem >= kGramPart && kGemmSmem >= 2 * kSmallMat, "smem");
 
@@ -66,6 +71,8 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem,
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ double block_sum(double x, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -441,8 +448,7 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
   const int wm = warp >> 1, wn = warp & 1;
   // ---------------- pass 1
   {
-    double* sA[2] = {sm, sm + kG1_A};
-    double* sB[2] = {sm + 2 * kG1_A, sm + 2 * kG1_A + kG1_B};
+    constexpr int kSt = kG1_A + kG1_B;  // one stage: A chunk, then VT chunk
     for (int rb = 0; rb < s; rb += kG1M) {
       const int kend = min(rb + kG1M, s);
       const int nk = (kend + kG1K - 1) / kG1K;
@@ -451,36 +457,38 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
       for (int a = 0; a < kMT1; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-      auto stage = [&](int kb, int buf) {
-        for (int t = tid; t < kG1M * (kG1K / 2); t += kNT) {
-          const int r = t >> 4, c2 = (t & 15) * 2;
-          const int gr = rb + r, gc = kb + c2;
-          int bytes = 0;
-          if (gr < s && gc < kend) bytes = (gc + 1 < kend) ? 16 : 8;
-          cp_async16(sA[buf] + r * kG1LDA + c2,
-                     bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
-        }
-        for (int t = tid; t < kG1K * (kB / 2); t += kNT) {
-          const int r = t >> 4, c2 = (t & 15) * 2;
-          const int gr = kb + r;
-          const int bytes = gr < kend ? 16 : 0;
-          cp_async16(sB[buf] + r * kG1LDB + c2,
-                     bytes ? VT + (long long)gr * kB + c2 : VT, bytes);
+      // one commit group per chunk (empty past the end) keeps the
+      // wait_group arithmetic uniform
+      auto stage = [&](int ki) {
+        if (ki < nk) {
+          const int kb = ki * kG1K, buf = ki % kG1S;
+          for (int t = tid; t < kG1M * (kG1K / 2); t += kNT) {
+            const int r = t >> 4, c2 = (t & 15) * 2;
+            const int gr = rb + r, gc = kb + c2;
+            int bytes = 0;
+            if (gr < s && gc < kend) bytes = (gc + 1 < kend) ? 16 : 8;
+            cp_async16(sm + buf * kSt + r * kG1LDA + c2,
+                       bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
+          }
+          for (int t = tid; t < kG1K * (kB / 2); t += kNT) {
+            const int r = t >> 4, c2 = (t & 15) * 2;
+            const int gr = kb + r;
+            const int bytes = gr < kend ? 16 : 0;
+            cp_async16(sm + buf * kSt + kG1_A + r * kG1LDB + c2,
+                       bytes ? VT + (long long)gr * kB + c2 : VT, bytes);
+          }
         }
         cpa_commit();
       };
       __syncthreads();
-      stage(0, 0);
+#pragma unroll
+      for (int p = 0; p < kG1S - 1; ++p) stage(p);
       for (int ki = 0; ki < nk; ++ki) {
-        if (ki + 1 < nk) {
-          stage((ki + 1) * kG1K, (ki + 1) & 1);
-          cpa_wait1();
-        } else {
-          cpa_wait0();
-        }
+        cpa_wait<kG1S - 2>();
         __syncthreads();
-        const double* a = sA[ki & 1];
-        const double* b = sB[ki & 1];
+        stage(ki + kG1S - 1);
+        const double* a = sm + (ki % kG1S) * kSt;
+        const double* b = a + kG1_A;
         const int kb = ki * kG1K;
         const bool diag = kb + kG1K > rb;  // chunk may cross the diagonal
 #pragma unroll
@@ -501,8 +509,8 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
             for (int nt = 0; nt < 2; ++nt)
               dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
         }
-        __syncthreads();
       }
+      cpa_wait0();
 #pragma unroll
       for (int mt = 0; mt < kMT1; ++mt) {
         const int r = rb + 8 * kMT1 * wm + 8 * mt + mm;
@@ -519,8 +527,7 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
   __syncthreads();
   // ---------------- pass 2
   {
-    double* sA[2] = {sm, sm + kG1_T};
-    double* sB[2] = {sm + 2 * kG1_T, sm + 2 * kG1_T + kG1_B};
+    constexpr int kSt = kG1_T + kG1_B;  // one stage: A chunk, then VT chunk
     for (int cb = 0; cb < s; cb += kG1M) {
       const int k0 = cb + 1;  // rows r > c >= cb
       if (k0 >= s) break;
@@ -542,36 +549,36 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
         }
       }
       const int cend = min(cb + kG1M, s);
-      auto stage = [&](int kb, int buf) {
-        for (int t = tid; t < kG1K * (kG1M / 2); t += kNT) {
-          const int r = t / (kG1M / 2), c2 = (t % (kG1M / 2)) * 2;
-          const int gr = kb + r, gc = cb + c2;
-          int bytes = 0;
-          if (gr < s && gc < cend) bytes = (gc + 1 < cend) ? 16 : 8;
-          cp_async16(sA[buf] + r * kG1TLD + c2,
-                     bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
-        }
-        for (int t = tid; t < kG1K * (kB / 2); t += kNT) {
-          const int r = t >> 4, c2 = (t & 15) * 2;
-          const int gr = kb + r;
-          const int bytes = gr < s ? 16 : 0;
-          cp_async16(sB[buf] + r * kG1LDB + c2,
-                     bytes ? VT + (long long)gr * kB + c2 : VT, bytes);
+      auto stage = [&](int ki) {
+        if (ki < nk) {
+          const int kb = k0 + ki * kG1K, buf = ki % kG1S;
+          for (int t = tid; t < kG1K * (kG1M / 2); t += kNT) {
+            const int r = t / (kG1M / 2), c2 = (t % (kG1M / 2)) * 2;
+            const int gr = kb + r, gc = cb + c2;
+            int bytes = 0;
+            if (gr < s && gc < cend) bytes = (gc + 1 < cend) ? 16 : 8;
+            cp_async16(sm + buf * kSt + r * kG1TLD + c2,
+                       bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
+          }
+          for (int t = tid; t < kG1K * (kB / 2); t += kNT) {
+            const int r = t >> 4, c2 = (t & 15) * 2;
+            const int gr = kb + r;
+            const int bytes = gr < s ? 16 : 0;
+            cp_async16(sm + buf * kSt + kG1_T + r * kG1LDB + c2,
+                       bytes ? VT + (long long)gr * kB + c2 : VT, bytes);
+          }
         }
         cpa_commit();
       };
       __syncthreads();
-      stage(k0, 0);
+#pragma unroll
+      for (int p = 0; p < kG1S - 1; ++p) stage(p);
       for (int ki = 0; ki < nk; ++ki) {
-        if (ki + 1 < nk) {
-          stage(k0 + (ki + 1) * kG1K, (ki + 1) & 1);
-          cpa_wait1();
-        } else {
-          cpa_wait0();
-        }
+        cpa_wait<kG1S - 2>();
         __syncthreads();
-        const double* a = sA[ki & 1];
-        const double* b = sB[ki & 1];
+        stage(ki + kG1S - 1);
+        const double* a = sm + (ki % kG1S) * kSt;
+        const double* b = a + kG1_T;
         const int kb = k0 + ki * kG1K;
         const bool diag = kb < cb + kG1M;
 #pragma unroll
@@ -592,8 +599,8 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
             for (int nt = 0; nt < 2; ++nt)
               dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
         }
-        __syncthreads();
       }
+      cpa_wait0();
 #pragma unroll
       for (int mt = 0; mt < kMT1; ++mt) {
         const int r = cb + 8 * kMT1 * wm + 8 * mt + mm;
@@ -612,113 +619,92 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
 
 // ---- GEMM 2: A22 -= W2 V^T + V W2^T on the lower triangle ----------------
 // As A22 += Aop Bop^T, Aop = -[W2 | V], Bop = [V | W2] (s x 2kB).  Row blocks
-// of 128 (Aop staged once), column blocks of 64 up to the diagonal (Bop
-// double-buffered by cp.async), C tiles prefetched into registers one tile
-// ahead.  Tiles crossing the diagonal also write their (never read) upper
-// part.
+// of 64: warp w owns rows 8w..8w+7 and keeps its Aop fragments (16 k-steps)
+// in registers for the whole row block; column tiles of 32 up to the
+// diagonal stream their C tile (HBM) and Bop rows (L2) through a kG2S-stage
+// cp.async pipeline in XOR-swizzled, unpadded shared memory, so two tiles
+// are in flight while one is computed.  Tiles crossing the diagonal also
+// write their (never read) upper part.
 __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
                       const double* V, double* sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
-  const int wm = warp >> 1, wn = warp & 1;
-  double* sOA = sm;
-  double* sOB[2] = {sm + kG2_A, sm + kG2_A + kG2_B};
-  auto load_c = [&](int rb, int cb, double (&c)[kMT2][kNT2][2]) {
-#pragma unroll
-    for (int mt = 0; mt < kMT2; ++mt) {
-      const int r = rb + 8 * kMT2 * wm + 8 * mt + mm;
-#pragma unroll
-      for (int nt = 0; nt < kNT2; ++nt) {
-        const int col = cb + 8 * kNT2 * wn + 8 * nt + 2 * kk;
-        if (r < s && col + 1 < s) {
-          // volatile: keeps the prefetch ahead of the (volatile) DMMAs of the
-          // current tile instead of letting the scheduler sink it to its use
-          asm volatile("ld.global.v2.f64 {%0, %1}, [%2];\n"
-                       : "=d"(c[mt][nt][0]), "=d"(c[mt][nt][1])
-                       : "l"(A22 + (long long)r * ldw + col));
-        } else {
-          c[mt][nt][0] = (r < s && col < s) ? A22[(long long)r * ldw + col] : 0.0;
-          c[mt][nt][1] = 0.0;
-        }
-      }
-    }
-  };
-  auto stage_b = [&](int cb, int buf) {
-    for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
-      const int r = t / (kG2K / 2), k2 = (t % (kG2K / 2)) * 2;
-      const int gr = cb + r;
-      const int bytes = gr < s ? 16 : 0;
-      const double* src = k2 < kB ? V + (long long)(bytes ? gr : 0) * kB + k2
-                                  : W2 + (long long)(bytes ? gr : 0) * kB + (k2 - kB);
-      cp_async16(sOB[buf] + r * kG2LD + k2, src, bytes);
-    }
-    cpa_commit();
-  };
+  const int crow = 8 * warp + mm;  // this lane's row within the row block
   for (int rb = 0; rb < s; rb += kG2M) {
-    __syncthreads();
-    for (int t = tid; t < kG2M * kG2K; t += kNT) {
-      const int r = t / kG2K, k = t % kG2K;
-      const int gr = rb + r;
-      double v = 0.0;
-      if (gr < s) v = k < kB ? W2[(long long)gr * kB + k] : V[(long long)gr * kB + k - kB];
-      sOA[r * kG2LD + k] = -v;
+    const int r = rb + crow;
+    double af[kG2K / 4];
+#pragma unroll
+    for (int k4 = 0; k4 < kG2K / 4; ++k4) {
+      const int k = 4 * k4 + kk;
+      af[k4] = r < s ? -(k < kB ? W2[(long long)r * kB + k] : V[(long long)r * kB + k - kB])
+                     : 0.0;
     }
     const int cend = min(rb + kG2M, s);
     const int ncb = (cend + kG2N - 1) / kG2N;
-    double cn[kMT2][kNT2][2];
-    load_c(rb, 0, cn);
-    stage_b(0, 0);
-    for (int ci = 0; ci < ncb; ++ci) {
-      const int cb = ci * kG2N;
-      double acc[kMT2][kNT2][2];
-#pragma unroll
-      for (int mt = 0; mt < kMT2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < kNT2; ++nt) {
-          acc[mt][nt][0] = cn[mt][nt][0];
-          acc[mt][nt][1] = cn[mt][nt][1];
+    auto stage = [&](int ci) {
+      if (ci < ncb) {
+        const int cb = ci * kG2N;
+        double* st = sm + (ci % kG2S) * kG2St;
+        for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
+          const int row = t >> 5, k2 = (t & 31) * 2;
+          const int gr = cb + row;
+          const int bytes = gr < s ? 16 : 0;
+          const long long g = (long long)(bytes ? gr : 0) * kB;
+          const double* src = k2 < kB ? V + g + k2 : W2 + g + (k2 - kB);
+          cp_async16(st + row * kG2K + (k2 ^ (4 * (row & 3))), src, bytes);
         }
-      if (ci + 1 < ncb) {
-        load_c(rb, cb + kG2N, cn);
-        stage_b(cb + kG2N, (ci + 1) & 1);
-        cpa_wait1();
-      } else {
-        cpa_wait0();
+        double* cs = st + kG2N * kG2K;
+        for (int t = tid; t < kG2M * (kG2N / 2); t += kNT) {
+          const int row = t >> 4, c2 = (t & 15) * 2;
+          const int gr = rb + row, gc = cb + c2;
+          int bytes = 0;
+          if (gr < s && gc < s) bytes = gc + 1 < s ? 16 : 8;
+          cp_async16(cs + row * kG2N + (c2 ^ (8 * (row & 1))),
+                     bytes ? A22 + (long long)gr * ldw + gc : A22, bytes);
+        }
       }
+      cpa_commit();
+    };
+    __syncthreads();  // the previous row block's last tile is consumed
+#pragma unroll
+    for (int p = 0; p < kG2S - 1; ++p) stage(p);
+    for (int ci = 0; ci < ncb; ++ci) {
+      cpa_wait<kG2S - 2>();
       __syncthreads();
-      const double* b = sOB[ci & 1];
-#pragma unroll 4
-      for (int k4 = 0; k4 < kG2K / 4; ++k4) {
-        const int kl = 4 * k4 + kk;
-        double af[kMT2], bf[kNT2];
+      stage(ci + kG2S - 1);
+      const double* b = sm + (ci % kG2S) * kG2St;
+      const double* cs = b + kG2N * kG2K;
+      double acc[kG2N / 8][2];
 #pragma unroll
-        for (int mt = 0; mt < kMT2; ++mt)
-          af[mt] = sOA[(8 * kMT2 * wm + 8 * mt + mm) * kG2LD + kl];
-#pragma unroll
-        for (int nt = 0; nt < kNT2; ++nt)
-          bf[nt] = b[(8 * kNT2 * wn + 8 * nt + mm) * kG2LD + kl];
-#pragma unroll
-        for (int mt = 0; mt < kMT2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < kNT2; ++nt)
-            dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+      for (int nt = 0; nt < kG2N / 8; ++nt) {
+        const double2 x = *reinterpret_cast<const double2*>(
+            cs + crow * kG2N + ((8 * nt + 2 * kk) ^ (8 * (crow & 1))));
+        acc[nt][0] = x.x;
+        acc[nt][1] = x.y;
       }
 #pragma unroll
-      for (int mt = 0; mt < kMT2; ++mt) {
-        const int r = rb + 8 * kMT2 * wm + 8 * mt + mm;
-        if (r >= s) continue;
+      for (int k4 = 0; k4 < kG2K / 4; ++k4) {
+        const int kl = (4 * k4 + kk) ^ (4 * (mm & 3));
+        double bf[kG2N / 8];
 #pragma unroll
-        for (int nt = 0; nt < kNT2; ++nt) {
-          const int col = cb + 8 * kNT2 * wn + 8 * nt + 2 * kk;
+        for (int nt = 0; nt < kG2N / 8; ++nt) bf[nt] = b[(8 * nt + mm) * kG2K + kl];
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[k4], bf[nt]);
+      }
+      if (r < s) {
+        const int cb = ci * kG2N;
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          const int col = cb + 8 * nt + 2 * kk;
           double* p = A22 + (long long)r * ldw + col;
           if (col + 1 < s)
-            *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+            *reinterpret_cast<double2*>(p) = make_double2(acc[nt][0], acc[nt][1]);
           else if (col < s)
-            p[0] = acc[mt][nt][0];
+            p[0] = acc[nt][0];
         }
       }
-      __syncthreads();
     }
+    cpa_wait0();
   }
   __syncthreads();
 }
@@ -757,13 +743,13 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
 #endif
   extern __shared__ double smem[];
   double* sgemm = smem;
-  double* sT = smem + kGemmSmem;
-  double* sG = sT + kSmallMat;   // G, then Y
+  double* sG = smem + kGemmSmem;  // G, then Y
   double* sA = sG + kSmallMat;
+  double* sT = sA + kSmallMat;
   double* sM = sA;               // M = T^T Y (A is dead by then)
   double* sB = sgemm;            // only alive between gram()/GEMM calls
   double* sR = sgemm + kSmallMat;
-  double* red = sA + kSmallMat;
+  double* red = sT + kSmallMat;
   double* stau = red + kRed;
   double* wsm = stau + kB;
   double* sS = wsm + kB;

@@ -10,10 +10,10 @@ import ctypes, sys, os, numpy as np
 sys.path.insert(0, os.getcwd())
 import paper_2002_04989_b200._native as nat
 lib = nat.load('/tmp/phb/libeigenid_b200.so')
-from oracle.oracle import Oracle
+from paper_2002_04989_b200.engine import random_symmetric
 from paper_2002_04989_b200 import IdentityEngine
 n = int(os.environ.get('N', '4096')); rows = int(os.environ.get('R', '147'))
-a = Oracle().random_symmetric(42, n) * np.sqrt(2.0 / n)
+a = random_symmetric(42, n) * np.sqrt(2.0 / n)
 eng = IdentityEngine()
 lam, mu = eng.minor_spectra(a, 0, rows)
 buf = (ctypes.c_ulonglong * 16)()
