@@ -26,81 +26,9 @@
 #include <vector>
 
 #include "../../include/eigenid_b200.h"
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace eigenid_b200 {
-// small.cu
-cudaError_t launch_small_all(const double* dA, size_t count, int n, int batch,
-                             double tol, int log_domain, double* dout,
-                             double* dlam, double* dmu, DevStatus* dstatus,
-                             cudaStream_t stream);
-// identity.cu
-int identity_nb(int n, int batch);
-cudaError_t launch_identity(const double* dlam, const double* dmu, int n,
-                            int rows, int batch, double* dden, double* drcp,
-                            double* dout, unsigned long long* dflag_count,
-                            long long* dflags, long long flag_cap,
-                            DevStatus* dstatus, int log_domain, cudaStream_t st,
-                            int* launches);
-cudaError_t launch_degeneracy(const double* dlam, int n, double tol,
-                              DevStatus* dstatus, cudaStream_t st,
-                              int* launches);
-cudaError_t launch_c5_mu(uint64_t seed, const double* dlam, int n, int j0,
-                         int rows, double* dmu, cudaStream_t st, int* launches);
-cudaError_t launch_component(const double* dlam, const double* dmu, int n,
-                             int i, int batch, double tol, int log_domain,
-                             double* dout3, DevStatus* dstatus, cudaStream_t st,
-                             int* launches);
-cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
-                          int batch, double* draw, DevStatus* dstatus,
-                          cudaStream_t st, int* launches);
-// band.cu
-struct Stage1Args {
-  const double* A;
-  int n;
-  const int* js;
-  int nsolves;
-  double* ws;
-  long long ws_stride;
-  int ldw;
-  double* band;
-  long long band_stride;
-};
-cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
-int stage1_band_ld();
-int stage1_bandwidth();
-// bulge.cu
-struct Stage2Args {
-  double* band;
-  long long band_stride;
-  const int* js;
-  int nsolves;
-  int n;
-  double* d;
-  double* e2;
-  double* ae;
-  long long de_stride;
-  int* counter;
-};
-cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st);
-// bisect.cu
-struct BisectArgs {
-  const double* d;
-  const double* e2;
-  const double* ae;
-  long long de_stride;
-  const int* js;
-  int nsolves;
-  int first_solve;
-  int n;
-  const double* lam;
-  double* out;
-  long long out_ld;
-  int split;
-};
-cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
-                          cudaStream_t st, int* launches);
-
 __global__ void init_status_kernel(DevStatus* st) {
   st[0].code = 0;
   st[0].phase = 0;
@@ -355,7 +283,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
     solve_list_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(djs, j0, (int)g0, cnt);
     ++launches;
     Stage1Args s1{dA, n, djs, cnt, c->bWs.as<double>(), ws_stride, ldw,
-                  c->bBand.as<double>(), band_stride};
+                  c->bBand.as<double>(), band_stride, c->bCounter.as<int>() + 1};
     EID_CUDA(launch_stage1(s1, cnt < slots ? cnt : slots, st), "stage1");
     ++launches;
     timer.mark(0);

@@ -17,7 +17,7 @@
 // of A (no host-side minor copies), the panel / T / W2 work is BLAS2-sized
 // and stays in L1/L2, and the band is written as kB+1.. 2kB+1 column-major
 // diagonals ready for the chase.
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace eigenid_b200 {
 
@@ -85,18 +85,6 @@ __device__ __forceinline__ double block_sum(double x, double* red) {
   for (int w = 0; w < kNT / 32; ++w) t += red[w];
   return t;
 }
-
-struct Stage1Args {
-  const double* A;    // n x n row-major
-  int n;
-  const int* js;      // solve list: js[s] = minor index, -1 = A itself
-  int nsolves;
-  double* ws;         // per-slot workspace
-  long long ws_stride;
-  int ldw;            // leading dimension of the slot matrix
-  double* band;       // per-solve band, column-major [col][0..2kB]
-  long long band_stride;
-};
 
 // ---- panel QR ----------------------------------------------------------
 // Householder QR of the s x kB panel P(r,q) = P0[r*ldw + q] (LAPACK
@@ -721,6 +709,12 @@ __device__ void write_band(const double* W, int ldw, int m, int c_begin,
 
 #ifdef EIGENID_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_cta_span[1536];  // per-CTA start, end, SM id
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 #define PHASE(id)                                                         \
   do {                                                                    \
     __syncthreads();                                                      \
@@ -740,6 +734,12 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
 #ifdef EIGENID_PHASE_TIMING
   long long t_ph_ = clock64();
   int ph_ = 0;
+  if (threadIdx.x == 0 && blockIdx.x < 512) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_cta_span[2 * blockIdx.x] = gtimer();
+    g_cta_span[1024 + blockIdx.x] = smid;
+  }
 #endif
   extern __shared__ double smem[];
   double* sgemm = smem;
@@ -761,7 +761,16 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
   double* VTg = Vg + (long long)n * kB;
   double* Xg = VTg + (long long)n * kB;
 
-  for (int sidx = blockIdx.x; sidx < args.nsolves; sidx += gridDim.x) {
+  // Solves are pulled from a work queue: the two CTAs sharing an SM do not
+  // progress at the same rate, so a static blockIdx stride leaves one of
+  // them running alone at the end of every wave.
+  __shared__ int s_sidx;
+  for (;;) {
+    if (tid == 0) s_sidx = atomicAdd(args.counter, 1);
+    __syncthreads();
+    const int sidx = s_sidx;
+    __syncthreads();
+    if (sidx >= args.nsolves) break;
     const int j = args.js[sidx];
     const int m = j < 0 ? n : n - 1;
     double* band = args.band + sidx * args.band_stride;
@@ -837,11 +846,17 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
     __syncthreads();
   }
   PHASE(0);
+#ifdef EIGENID_PHASE_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 512) g_cta_span[2 * blockIdx.x + 1] = gtimer();
+#endif
 }
 
 #ifdef EIGENID_PHASE_TIMING
 extern "C" void eigenid_debug_phase_cycles(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+}
+extern "C" void eigenid_debug_cta_span(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_cta_span, sizeof(g_cta_span));
 }
 #endif
 
@@ -853,6 +868,8 @@ cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st) {
   const size_t smem = stage1_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(
       band_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   band_reduce_kernel<<<grid, kNT, smem, st>>>(a);
   return cudaGetLastError();

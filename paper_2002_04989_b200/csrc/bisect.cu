@@ -9,26 +9,11 @@
 // One CTA per minor stages (d, e^2) in shared memory (64 KB at m = 4095);
 // one thread per eigenvalue, so every Sturm step of a warp is a broadcast
 // shared-memory read.
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace eigenid_b200 {
 
 constexpr int kBisNT = 256;
-
-struct BisectArgs {
-  const double* d;
-  const double* e2;
-  const double* ae;
-  long long de_stride;
-  const int* js;
-  int nsolves;
-  int first_solve;       // solve index of the first CTA (blockIdx.x offset)
-  int n;
-  const double* lam;     // interlacing brackets (nullptr: Gershgorin only)
-  double* out;           // row r = solve first_solve + r ... see out_ld
-  long long out_ld;
-  int split;             // CTAs per solve (eigenvalue ranges), >= 1
-};
 
 __device__ double block_reduce_max(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -21,7 +21,7 @@
 // step k+1 are prefetched while step k computes (C into registers, lane =
 // row; the full symmetric D into a shared-memory double buffer by cp.async).
 // CTAs pull solves from an atomic work counter (persistent kernel).
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace eigenid_b200 {
 
@@ -31,19 +31,6 @@ constexpr int kWarpsPerCta = 8;
 constexpr int kSLD = kCB + 1;
 constexpr int kBlk = kCB * kSLD;
 constexpr int kWarpSmem = 3 * kBlk + 3 * kCB;  // sC, sD[2], v, v2, w
-
-struct Stage2Args {
-  double* band;            // per solve: m columns x kCLD
-  long long band_stride;
-  const int* js;           // -1 = A itself (m = n), else m = n - 1
-  int nsolves;
-  int n;
-  double* d;               // per solve: m diagonal
-  double* e2;              // per solve: m-1 squared off-diagonal
-  double* ae;              // per solve: m-1 |off-diagonal|
-  long long de_stride;
-  int* counter;            // work queue (zeroed before launch)
-};
 
 __device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool ok) {
   const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);

@@ -19,7 +19,7 @@
 //    (8 warps x 4 rows); mu for the 32 rows is staged through shared memory
 //    in 64-wide k chunks with cp.async double buffering; inside a warp every
 //    mu load is a broadcast.
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace eigenid_b200 {
 

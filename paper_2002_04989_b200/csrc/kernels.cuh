@@ -1,0 +1,91 @@
+// kernels.cuh — launch interfaces of the device stages, shared by the
+// kernel files and the pipeline in api.cu (one definition per argument
+// struct, so the two sides cannot drift apart).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace eigenid_b200 {
+
+// ---- small.cu: whole pipeline for n <= 64
+cudaError_t launch_small_all(const double* dA, size_t count, int n, int batch,
+                             double tol, int log_domain, double* dout,
+                             double* dlam, double* dmu, DevStatus* dstatus,
+                             cudaStream_t stream);
+
+// ---- band.cu: stage 1, dense -> band
+struct Stage1Args {
+  const double* A;    // n x n row-major
+  int n;
+  const int* js;      // solve list: js[s] = minor index, -1 = A itself
+  int nsolves;
+  double* ws;         // per-slot workspace
+  long long ws_stride;
+  int ldw;            // leading dimension of the slot matrix
+  double* band;       // per-solve band, column-major [col][0..2kB]
+  long long band_stride;
+  int* counter;       // work queue (zeroed before launch)
+};
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
+int stage1_band_ld();
+int stage1_bandwidth();
+
+// ---- bulge.cu: stage 2, band -> tridiagonal
+struct Stage2Args {
+  double* band;            // per solve: m columns x kCLD
+  long long band_stride;
+  const int* js;           // -1 = A itself (m = n), else m = n - 1
+  int nsolves;
+  int n;
+  double* d;               // per solve: m diagonal
+  double* e2;              // per solve: m-1 squared off-diagonal
+  double* ae;              // per solve: m-1 |off-diagonal|
+  long long de_stride;
+  int* counter;            // work queue (zeroed before launch)
+};
+cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st);
+
+// ---- bisect.cu: Sturm bisection of the tridiagonals
+struct BisectArgs {
+  const double* d;
+  const double* e2;
+  const double* ae;
+  long long de_stride;
+  const int* js;
+  int nsolves;
+  int first_solve;       // solve index of the first CTA (blockIdx.x offset)
+  int n;
+  const double* lam;     // interlacing brackets (nullptr: Gershgorin only)
+  double* out;           // row r = solve first_solve + r ... see out_ld
+  long long out_ld;
+  int split;             // CTAs per solve (eigenvalue ranges), >= 1
+};
+cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
+                          cudaStream_t st, int* launches);
+
+// ---- identity.cu
+int identity_nb(int n, int batch);
+cudaError_t launch_identity(const double* dlam, const double* dmu, int n,
+                            int rows, int batch, double* dden, double* drcp,
+                            double* dout, unsigned long long* dflag_count,
+                            long long* dflags, long long flag_cap,
+                            DevStatus* dstatus, int log_domain, cudaStream_t st,
+                            int* launches);
+cudaError_t launch_degeneracy(const double* dlam, int n, double tol,
+                              DevStatus* dstatus, cudaStream_t st,
+                              int* launches);
+cudaError_t launch_c5_mu(uint64_t seed, const double* dlam, int n, int j0,
+                         int rows, double* dmu, cudaStream_t st, int* launches);
+cudaError_t launch_component(const double* dlam, const double* dmu, int n,
+                             int i, int batch, double tol, int log_domain,
+                             double* dout3, DevStatus* dstatus, cudaStream_t st,
+                             int* launches);
+cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
+                          int batch, double* draw, DevStatus* dstatus,
+                          cudaStream_t st, int* launches);
+
+}  // namespace eigenid_b200

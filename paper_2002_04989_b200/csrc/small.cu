@@ -15,7 +15,7 @@
 // A, lambda and all n minor spectra never leave shared memory; HBM traffic is
 // A in (8 n^2 B) and |v|^2 out (8 n^2 B) per matrix.  Config C2 (4096 x n=32)
 // runs 4096 CTAs; C1 (n=64) one.
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace eigenid_b200 {
 

@@ -22,6 +22,21 @@ names = ['other', 'copy', 'panel', 'band+VT', 'gemm1', 'Y,M,W2', 'gemm2', '-']
 tot = sum(buf[i] for i in range(8))
 print('stage 1 (CTA 0):')
 for i in range(8): print(f'  {names[i]:10s} {buf[i]/1.965e9*1e3:9.2f} ms  {100*buf[i]/max(tot,1):5.1f}%')
+sp = (ctypes.c_ulonglong * 1536)()
+lib.eigenid_debug_cta_span(sp)
+g = min(rows + 1, 296)
+st = np.array([sp[2 * b] for b in range(g)], dtype=np.float64)
+sm = np.array([sp[1024 + b] for b in range(g)])
+en = np.array([sp[2 * b + 1] for b in range(g)], dtype=np.float64)
+t0 = st.min()
+dur = (en - st) / 1e6
+print(f'stage 1 CTA spans (ms): start max {(st.max()-t0)/1e6:.2f}  dur min {dur.min():.1f} '
+      f'median {np.median(dur):.1f} max {dur.max():.1f}')
+order = np.argsort(dur)
+print('  fastest (cta, sm, ms):', [(int(b), int(sm[b]), round(float(dur[b]), 1)) for b in order[:6]])
+print('  slowest (cta, sm, ms):', [(int(b), int(sm[b]), round(float(dur[b]), 1)) for b in order[-6:]])
+hist = np.histogram(dur, bins=8)
+print('  hist:', [int(x) for x in hist[0]], [round(float(x), 0) for x in hist[1]])
 b2 = (ctypes.c_ulonglong * 8)()
 lib.eigenid_debug_bulge_cycles(b2)
 names = ['loop/sweep', 'prefetch issue', 'right-apply+hh', 'left-apply+C store', 'wait D', 'two-sided+store', 'wait prev sweep']
