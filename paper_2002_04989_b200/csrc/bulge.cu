@@ -19,7 +19,8 @@
 // band traffic to HBM drops ~8x versus independent solves per warp.  Within
 // a sweep a step never reads what the previous step wrote, so the blocks of
 // step k+1 are prefetched while step k computes (C into registers, lane =
-// row; the full symmetric D into a shared-memory double buffer by cp.async).
+// row; the lower triangle of D into a shared-memory double buffer by
+// cp.async, one coalesced run per column).
 // CTAs pull solves from an atomic work counter (persistent kernel).
 #include "kernels.cuh"
 
@@ -73,9 +74,9 @@ __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
   return tau;
 }
 
-// D <- H D H on the L x L diagonal block held (both triangles) in sD
-// (filled by cp.async; rows/cols >= L are zero).  Writes the lower triangle
-// back to the band.
+// D <- H D H on the L x L diagonal block whose lower triangle is held in sD
+// (filled by cp.async; rows/cols >= L are zero; the upper triangle is read
+// through the mirror).  Writes the lower triangle back to the band.
 __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
                                                 double tau, double* sw, int L,
                                                 double* AB, int R) {
@@ -84,7 +85,7 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
   double pp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < kCB; ++c) {
-    drow[c] = sD[lane * kSLD + c];
+    drow[c] = sD[c <= lane ? lane * kSLD + c : c * kSLD + lane];
     pp[c & 3] += drow[c] * sv[c];
   }
   double p = (pp[0] + pp[1]) + (pp[2] + pp[3]);
@@ -106,16 +107,17 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
 
 __device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
                                            int L) {
-  // full symmetric L x L block: element (r, c) lives at column min(r,c),
-  // diagonal |r - c| of the band; out-of-range entries are zero-filled
+  // lower triangle of the L x L block: element (r, c), r >= c, lives at
+  // column c, diagonal r - c of the band (one coalesced run per column);
+  // out-of-range entries are zero-filled
   const int lane = threadIdx.x & 31;
-  const double* base = AB + (long long)R * kCLD;
+  const double* base = AB + (long long)R * kCLD + lane;
 #pragma unroll
   for (int c = 0; c < kCB; ++c) {
-    const bool ok = lane < L && c < L;
-    // (r, c) -> column min(r,c), diagonal |r-c|
-    const int off = (c <= lane) ? c * kCLD + (lane - c) : lane * kCLD + (c - lane);
-    cpa8(sD + lane * kSLD + c, ok ? base + off : AB, ok);
+    if (lane >= c) {
+      const bool ok = lane < L;
+      cpa8(sD + lane * kSLD + c, ok ? base + c * (kCLD - 1) : AB, ok);
+    }
   }
   cpa_commit2();
 }
