@@ -86,9 +86,12 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load(path: str = LIB_PATH):
-    """Loads the CUDA library (raises DeviceError if it was not built)."""
+def load(path: str | None = None):
+    """Loads the CUDA library (raises DeviceError if it was not built).
+    EIGENID_LIB selects another build of the same library (A/B timing of
+    kernel variants, tools/variant_run.sh)."""
     global _lib
+    path = path or os.environ.get("EIGENID_LIB") or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

@@ -11,16 +11,17 @@
 // position, so a step touches only C and D (band storage keeps 2kB+1
 // diagonals per column).
 //
-// A CTA owns one solve at a time and its 8 warps chase 8 consecutive sweeps
-// concurrently (warp w takes sweeps w, w+8, ...): sweep s may run step k once
+// A CTA owns one solve at a time and its 8 warps chase 8 consecutive
+// sweeps concurrently (warp w takes sweeps w, w+8, ...): sweep s may run step k once
 // sweep s-1 has finished step k+1 (k+2 before prefetching step k+1), tracked
 // by per-warp progress counters in shared memory.  The leading sweep pulls
-// each block from HBM and the 7 following sweeps re-read it from L2/L1, so
-// band traffic to HBM drops ~8x versus independent solves per warp.  Within
+// each block from HBM and the following sweeps re-read it from L2/L1, so
+// band traffic to HBM drops ~8x versus independent solves per warp (12
+// warps measured slower: 168 registers per thread and a smaller L1).  Within
 // a sweep a step never reads what the previous step wrote, so the blocks of
-// step k+1 are prefetched while step k computes (C into registers, lane =
-// row; the lower triangle of D into a shared-memory double buffer by
-// cp.async, one coalesced run per column).
+// step k+1 are prefetched by cp.async while step k computes: the lower
+// triangle of D (packed) into a double buffer, C into the transposition
+// buffer once step k's left-apply has consumed it.
 // CTAs pull solves from an atomic work counter (persistent kernel).
 #include "kernels.cuh"
 
@@ -28,10 +29,17 @@ namespace eigenid_b200 {
 
 constexpr int kCB = 32;              // bandwidth (must match band.cu kB)
 constexpr int kCLD = 2 * kCB + 1;    // band diagonals stored per column
-constexpr int kWarpsPerCta = 8;
+#ifndef EIGENID_BULGE_WARPS
+#define EIGENID_BULGE_WARPS 8
+#endif
+constexpr int kWarpsPerCta = EIGENID_BULGE_WARPS;
 constexpr int kSLD = kCB + 1;
 constexpr int kBlk = kCB * kSLD;
-constexpr int kWarpSmem = 3 * kBlk + 3 * kCB;  // sC, sD[2], v, v2, w
+constexpr int kDP = kCB * (kCB + 1) / 2;        // packed lower triangle of D
+constexpr int kWarpSmem = kBlk + 2 * kDP + 3 * kCB;  // sC, sD[2], v, v2, w
+
+// Row-packed lower triangle: (r, c), r >= c.
+__device__ __forceinline__ int dp(int r, int c) { return (r * (r + 1) >> 1) + c; }
 
 __device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool ok) {
   const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
@@ -85,7 +93,7 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
   double pp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < kCB; ++c) {
-    drow[c] = sD[c <= lane ? lane * kSLD + c : c * kSLD + lane];
+    drow[c] = sD[c <= lane ? dp(lane, c) : dp(c, lane)];
     pp[c & 3] += drow[c] * sv[c];
   }
   double p = (pp[0] + pp[1]) + (pp[2] + pp[3]);
@@ -116,19 +124,24 @@ __device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
   for (int c = 0; c < kCB; ++c) {
     if (lane >= c) {
       const bool ok = lane < L;
-      cpa8(sD + lane * kSLD + c, ok ? base + c * (kCLD - 1) : AB, ok);
+      cpa8(sD + dp(lane, c), ok ? base + c * (kCLD - 1) : AB, ok);
     }
   }
   cpa_commit2();
 }
 
-__device__ __forceinline__ void load_c(double (&cr)[kCB], const double* AB,
-                                       int R1, int L1, int R, int L) {
+// C = A[R1.., R..] (L1 x L) into sC (row r = lane, padded rows); one
+// coalesced run per column, out-of-range entries zero-filled.
+__device__ __forceinline__ void prefetch_c(double* sC, const double* AB, int R1,
+                                           int L1, int R, int L) {
   const int lane = threadIdx.x & 31;
   const double* base = AB + (long long)R * kCLD + (R1 - R) + lane;
 #pragma unroll
-  for (int c = 0; c < kCB; ++c)
-    cr[c] = (lane < L1 && c < L) ? base[c * (kCLD - 1)] : 0.0;
+  for (int c = 0; c < kCB; ++c) {
+    const bool ok = lane < L1 && c < L;
+    cpa8(sC + lane * kSLD + c, ok ? base + c * (kCLD - 1) : AB, ok);
+  }
+  cpa_commit2();
 }
 
 #ifdef EIGENID_PHASE_TIMING
@@ -150,7 +163,8 @@ __device__ __forceinline__ long long spos(int sweep, int step) {
   return (long long)sweep * 65536 + step;
 }
 
-// Blocks until sweep s-1 (owned by warp (w-1) mod 8) has finished step k.
+// Blocks until sweep s-1 (owned by warp w-1 mod kWarpsPerCta) has finished
+// step k.
 __device__ __forceinline__ void wait_prev(volatile long long* prog, int warp,
                                           int s, int k) {
   if (s == 0) return;
@@ -179,8 +193,8 @@ bulge_chase_kernel(Stage2Args a) {
   __shared__ int s_sidx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sC = smem + warp * kWarpSmem;
-  double* sDb[2] = {sC + kBlk, sC + 2 * kBlk};
-  double* sv = sC + 3 * kBlk;
+  double* const sD0 = sC + kBlk;  // D double buffer: sD0 + buf * kDP
+  double* sv = sC + kBlk + 2 * kDP;
   double* sv2 = sv + kCB;
   double* sw = sv2 + kCB;
 
@@ -203,25 +217,27 @@ bulge_chase_kernel(Stage2Args a) {
       // block 0 and the prefetch of step 1 need sweep st-1 past step 2
       wait_prev(prog, warp, st, 2);
       const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
-      prefetch_d(sDb[0], AB, R0, L0);
-      double ncrow[kCB];
+      prefetch_d(sD0, AB, R0, L0);
       if (have) {
-        load_c(ncrow, AB, Rk, Lk, R0, L0);
-        prefetch_d(sDb[1], AB, Rk, Lk);
+        prefetch_d(sD0 + kDP, AB, Rk, Lk);
+        prefetch_c(sC, AB, Rk, Lk, R0, L0);
       }
       double beta;
       double tau = warp_householder(x, L0, sv, &beta);
       if (lane < L0) AB[(long long)st * kCLD + 1 + lane] = (lane == 0) ? beta : 0.0;
-      if (have) cpa_wait_one(); else cpa_wait_all();
+      cpa_wait_all();
       __syncwarp();
-      two_sided_store(sDb[0], sv, tau, sw, L0, AB, R0);
+      two_sided_store(sD0, sv, tau, sw, L0, AB, R0);
       publish(prog, warp, st, 0);
       int R = R0, L = L0, buf = 1, k = 1;
       while (have) {
-        // ---- step k on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]
+        // ---- step k on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]; both
+        // were prefetched during step k-1
+        cpa_wait_all();
+        __syncwarp();
         double crow[kCB];
 #pragma unroll
-        for (int c = 0; c < kCB; ++c) crow[c] = ncrow[c];
+        for (int c = 0; c < kCB; ++c) crow[c] = sC[lane * kSLD + c];
         const int Rn = Rk + kCB;
         const bool haven = Rn <= m - 1;
         const int Ln = haven ? min(kCB, m - Rn) : 0;
@@ -229,8 +245,7 @@ bulge_chase_kernel(Stage2Args a) {
         if (haven) {
           wait_prev(prog, warp, st, k + 2);
           BPH(6);
-          load_c(ncrow, AB, Rn, Ln, Rk, Lk);
-          prefetch_d(sDb[buf ^ 1], AB, Rn, Ln);
+          prefetch_d(sD0 + (buf ^ 1) * kDP, AB, Rn, Ln);
         }
         BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
@@ -257,6 +272,9 @@ bulge_chase_kernel(Stage2Args a) {
           sw[lane] = (lane >= 1 && lane < L) ? tau2 * w : 0.0;
         }
         __syncwarp();
+        // sC is free again: next step's C block lands during the two-sided
+        // update below
+        if (haven) prefetch_c(sC, AB, Rn, Ln, Rk, Lk);
         {
           const double vr = sv2[lane];
 #pragma unroll
@@ -269,11 +287,8 @@ bulge_chase_kernel(Stage2Args a) {
             st_pred(base + c * (kCLD - 1), crow[c], lane < Lk && c < L);
         }
         BPH(3);
-        // two-sided on the diagonal block (prefetched into sDb[buf])
-        if (haven) cpa_wait_one(); else cpa_wait_all();
-        __syncwarp();
         BPH(4);
-        two_sided_store(sDb[buf], sv2, tau2, sw, Lk, AB, Rk);
+        two_sided_store(sD0 + buf * kDP, sv2, tau2, sw, Lk, AB, Rk);
         BPH(5);
         sv[lane] = sv2[lane];
         publish(prog, warp, st, k);
