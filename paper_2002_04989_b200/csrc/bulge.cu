@@ -91,10 +91,14 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
   const int lane = threadIdx.x & 31;
   double drow[kCB];
   double pp[4] = {0.0, 0.0, 0.0, 0.0};
+  const double2* v2 = reinterpret_cast<const double2*>(sv);
 #pragma unroll
-  for (int c = 0; c < kCB; ++c) {
-    drow[c] = sD[c <= lane ? dp(lane, c) : dp(c, lane)];
-    pp[c & 3] += drow[c] * sv[c];
+  for (int c = 0; c < kCB; ++c) drow[c] = sD[c <= lane ? dp(lane, c) : dp(c, lane)];
+#pragma unroll
+  for (int h = 0; h < kCB / 2; ++h) {  // broadcast reads, two per LDS.128
+    const double2 v = v2[h];
+    pp[(2 * h) & 3] += drow[2 * h] * v.x;
+    pp[(2 * h + 1) & 3] += drow[2 * h + 1] * v.y;
   }
   double p = (pp[0] + pp[1]) + (pp[2] + pp[3]);
   p *= tau;
@@ -103,8 +107,13 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
   const double w = p - K * vr;
   sw[lane] = w;
   __syncwarp();
+  const double2* w2 = reinterpret_cast<const double2*>(sw);
 #pragma unroll
-  for (int c = 0; c < kCB; ++c) drow[c] -= vr * sw[c] + w * sv[c];
+  for (int h = 0; h < kCB / 2; ++h) {
+    const double2 a = w2[h], v = v2[h];
+    drow[2 * h] -= vr * a.x + w * v.x;
+    drow[2 * h + 1] -= vr * a.y + w * v.y;
+  }
   // lower triangle back to the band: column c, rows c..L-1 (coalesced in r)
   double* base = AB + (long long)R * kCLD + lane;
 #pragma unroll
@@ -249,12 +258,21 @@ bulge_chase_kernel(Stage2Args a) {
         }
         BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
+        const double2* v2 = reinterpret_cast<const double2*>(sv);
         double yy[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int c = 0; c < kCB; ++c) yy[c & 3] += crow[c] * sv[c];
+        for (int h = 0; h < kCB / 2; ++h) {
+          const double2 v = v2[h];
+          yy[(2 * h) & 3] += crow[2 * h] * v.x;
+          yy[(2 * h + 1) & 3] += crow[2 * h + 1] * v.y;
+        }
         const double y = tau * ((yy[0] + yy[1]) + (yy[2] + yy[3]));
 #pragma unroll
-        for (int c = 0; c < kCB; ++c) crow[c] -= y * sv[c];
+        for (int h = 0; h < kCB / 2; ++h) {
+          const double2 v = v2[h];
+          crow[2 * h] -= y * v.x;
+          crow[2 * h + 1] -= y * v.y;
+        }
         // new reflector from C's first column
         double beta2;
         const double tau2 = warp_householder(crow[0], Lk, sv2, &beta2);
@@ -265,9 +283,14 @@ bulge_chase_kernel(Stage2Args a) {
         for (int c = 0; c < kCB; ++c) sC[lane * kSLD + c] = crow[c];
         __syncwarp();
         {
+          const double2* u2 = reinterpret_cast<const double2*>(sv2);
           double ww[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int r = 0; r < kCB; ++r) ww[r & 3] += sv2[r] * sC[r * kSLD + lane];
+          for (int h = 0; h < kCB / 2; ++h) {
+            const double2 u = u2[h];
+            ww[(2 * h) & 3] += u.x * sC[(2 * h) * kSLD + lane];
+            ww[(2 * h + 1) & 3] += u.y * sC[(2 * h + 1) * kSLD + lane];
+          }
           const double w = (ww[0] + ww[1]) + (ww[2] + ww[3]);
           sw[lane] = (lane >= 1 && lane < L) ? tau2 * w : 0.0;
         }
@@ -277,8 +300,13 @@ bulge_chase_kernel(Stage2Args a) {
         if (haven) prefetch_c(sC, AB, Rn, Ln, Rk, Lk);
         {
           const double vr = sv2[lane];
+          const double2* w2 = reinterpret_cast<const double2*>(sw);
 #pragma unroll
-          for (int c = 1; c < kCB; ++c) crow[c] -= vr * sw[c];
+          for (int h = 0; h < kCB / 2; ++h) {
+            const double2 a = w2[h];
+            if (h > 0) crow[2 * h] -= vr * a.x;  // w_0 = 0: column 0 is final
+            crow[2 * h + 1] -= vr * a.y;
+          }
         }
         {
           double* base = AB + (long long)R * kCLD + (Rk - R) + lane;
