@@ -228,31 +228,52 @@ __device__ void gram(const double* L, int ldl, const double* R, int ldr, int s,
   __syncthreads();
 }
 
-// Y(r,:) = (Add ? Add(r,:) : 0) + alpha * L(r,:) Mt, warp per row, lane per
-// output column (Mt in shared memory, ld kSmallLD).  In place is allowed.
+// Y(r,:) = (Add ? Add(r,:) : 0) + alpha * L(r,:) Mt (Mt kB x kB in shared
+// memory, ld kSmallLD) on the DMMA path: warp w owns the 32-row blocks
+// w, w+8, ... and keeps the 32 x 32 output block in registers, so Y may alias
+// L or Add.
 __device__ void row_transform(const double* L, int ldl, const double* Mt,
                               double alpha, const double* Add, double* Y,
                               int s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r0 = warp; r0 < s; r0 += 2 * (kNT / 32)) {
-    double l[2], y[2] = {0.0, 0.0};
+  const int kk = lane & 3, mm = lane >> 2;
+  for (int rb = 32 * warp; rb < s; rb += 32 * (kNT / 32)) {
+    double acc[4][4][2];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = r0 + 8 * u;
-      l[u] = r < s ? L[(long long)r * ldl + lane] : 0.0;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 2
+    for (int k4 = 0; k4 < kB / 4; ++k4) {
+      const int k = 4 * k4 + kk;
+      double af[4], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int r = rb + 8 * mt + mm;
+        af[mt] = r < s ? L[(long long)r * ldl + k] : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Mt[k * kSmallLD + 8 * nt + mm];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
     }
 #pragma unroll
-    for (int p = 0; p < kB; ++p) {
-      const double mv = Mt[p * kSmallLD + lane];
+    for (int mt = 0; mt < 4; ++mt) {
+      const int r = rb + 8 * mt + mm;
+      if (r >= s) continue;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) y[u] += __shfl_sync(0xffffffffu, l[u], p) * mv;
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = r0 + 8 * u;
-      if (r < s)
-        Y[(long long)r * kB + lane] =
-            (Add ? Add[(long long)r * kB + lane] : 0.0) + alpha * y[u];
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = 8 * nt + 2 * kk;
+        double2 y = make_double2(alpha * acc[mt][nt][0], alpha * acc[mt][nt][1]);
+        if (Add) {
+          const double2 ad = *reinterpret_cast<const double2*>(Add + (long long)r * kB + c);
+          y.x += ad.x;
+          y.y += ad.y;
+        }
+        *reinterpret_cast<double2*>(Y + (long long)r * kB + c) = y;
+      }
     }
   }
   __syncthreads();
@@ -335,11 +356,32 @@ __device__ void warp_upper_mul(const double* A, const double* B, double* C) {
   __syncwarp();
 }
 
+#ifdef EIGENID_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+// sub-phases of chol_panel (CTA 0) -> g_phase_cycles[8 + id]
+#define SUBPH(id)                                                          \
+  do {                                                                     \
+    __syncthreads();                                                       \
+    const long long now_ = clock64();                                      \
+    if (threadIdx.x == 0 && blockIdx.x == 0)                               \
+      atomicAdd(&g_phase_cycles[8 + (id)], (unsigned long long)(now_ - t_sp_)); \
+    t_sp_ = now_;                                                          \
+  } while (0)
+#else
+#define SUBPH(id) \
+  do {            \
+  } while (0)
+#endif
+
 __device__ bool chol_panel(double* P0, int ldw, int s, double* Vg, double* Xg,
                            double* sT, double* sG, double* sA, double* sB,
                            double* sR, double* sS, double* part, int* flag) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef EIGENID_PHASE_TIMING
+  long long t_sp_ = clock64();
+#endif
   gram(P0, ldw, P0, ldw, s, sG, part);                    // G1 = P^T P
+  SUBPH(0);
   if (warp == 0) {
     const bool ok = warp_chol(sG, sA);                     // R1
     if (lane == 0) *flag = ok;
@@ -347,8 +389,11 @@ __device__ bool chol_panel(double* P0, int ldw, int s, double* Vg, double* Xg,
   }
   __syncthreads();
   if (!*flag) return false;
+  SUBPH(1);
   row_transform(P0, ldw, sB, 1.0, nullptr, Vg, s);         // Q = P R1^-1
+  SUBPH(2);
   gram(Vg, kB, Vg, kB, s, sG, part);                      // G2 = Q^T Q
+  SUBPH(3);
   if (warp == 0) {
     double dev = 0.0;
     for (int e = lane; e < kB * kB; e += 32) {
@@ -366,7 +411,9 @@ __device__ bool chol_panel(double* P0, int ldw, int s, double* Vg, double* Xg,
   }
   __syncthreads();
   if (!*flag) return false;
+  SUBPH(4);
   row_transform(Vg, kB, sA, 1.0, nullptr, Xg, s);          // Q1 = Q R2^-1
+  SUBPH(5);
   if (warp == 0) {
     // modified LU of the top block: Q1_top - S = L U (U' in sG upper)
     for (int r = 0; r < kB; ++r) sG[r * kSmallLD + lane] = Xg[r * kB + lane];
@@ -420,7 +467,9 @@ __device__ bool chol_panel(double* P0, int ldw, int s, double* Vg, double* Xg,
   for (int r = warp; r < kB; r += kNT / 32)
     P0[(long long)r * ldw + lane] = lane >= r ? sS[r] * sR[r * kSmallLD + lane] : 0.0;
   __syncthreads();
+  SUBPH(6);
   row_transform(Xg + kB * kB, kB, sB, 1.0, nullptr, Vg + kB * kB, s - kB);
+  SUBPH(2);
   return true;
 }
 
@@ -708,7 +757,6 @@ __device__ void write_band(const double* W, int ldw, int m, int c_begin,
 }
 
 #ifdef EIGENID_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[16];
 __device__ unsigned long long g_cta_span[1536];  // per-CTA start, end, SM id
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -804,6 +852,9 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
                         chol_panel(P0, ldw, s, Vg, Xg, sT, sG, sA, sB, sR, sS,
                                    sgemm, sflag);
       if (!fast) {
+#ifdef EIGENID_PHASE_TIMING
+        if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_phase_cycles[15], 1ull);
+#endif
         panel_qr(P0, ldw, s, stau, red, wsm);
         extract_v(P0, ldw, s, Vg);
         // T (dlarft, forward columnwise) from G = V^T V
