@@ -243,7 +243,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   const int kB = stage1_bandwidth();
   const int ldab = stage1_band_ld();
   const int ldw = (n + 7) & ~7;
-  const long long ws_stride = (long long)n * ldw + 3LL * n * kB;
+  const long long ws_stride = stage1_ws_doubles(n, ldw);
   const long long band_stride = (long long)n * ldab;
   // Memory plan: stage-1 workspace slots and the number of solves whose band
   // and tridiagonal are resident at once, sized to the free device memory

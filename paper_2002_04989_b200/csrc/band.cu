@@ -40,12 +40,24 @@ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int kG1S = 3;                             // GEMM 1 cp.async stages
 constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
 constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
-constexpr int kGemmSmem = cmax(kGramPart, kG2S * kG2St - 3 * kSmallMat);
+#ifndef EIGENID_STAGE1_FUSED
+#define EIGENID_STAGE1_FUSED 1
+#endif
+// Fused pass (rest of panel p's update + SYMM of panel p+1): two stages of
+// {Bop rows, C tile, VT(cb) rows} plus the row block's VT(rb) rows.
+constexpr int kFVLD = 34, kFVRLD = 36;
+constexpr int kFSt = kG2N * kG2K + kG2M * kG2N + kB * kFVLD;
+constexpr int kFSmem = 2 * kFSt + kG2M * kFVRLD;
+constexpr int kGemmSmem =
+    cmax(cmax(kGramPart, kG2S * kG2St - 3 * kSmallMat),
+         EIGENID_STAGE1_FUSED ? kFSmem - 2 * kSmallMat : 0);
 // GEMM 1 also owns the G and A scratch matrices that follow the GEMM region
 // (both dead while it runs; T, after them, is not).
 constexpr int kGemm1Smem = kGemmSmem + 2 * kSmallMat;
 // GEMM 2 owns G, A and T as well (all dead while it runs).
 static_assert(kG2S * kG2St <= kGemmSmem + 3 * kSmallMat, "gemm2 smem");
+// the fused pass owns G and A but not T (T of panel p+1 outlives it)
+static_assert(!EIGENID_STAGE1_FUSED || kFSmem <= kGemmSmem + 2 * kSmallMat, "fused smem");
 static_assert(kG1S * (kG1_A + kG1_B) <= kGemm1Smem &&
                   kG1S * (kG1_T + kG1_B) <= kGemm1Smem, "gemm1 smem");
 constexpr int kRed = 8 + 8 * kB;
@@ -363,7 +375,7 @@ __device__ unsigned long long g_phase_cycles[16];
   do {                                                                     \
     __syncthreads();                                                       \
     const long long now_ = clock64();                                      \
-    if (threadIdx.x == 0 && blockIdx.x == 0)                               \
+    if (threadIdx.x == 0)                                                  \
       atomicAdd(&g_phase_cycles[8 + (id)], (unsigned long long)(now_ - t_sp_)); \
     t_sp_ = now_;                                                          \
   } while (0)
@@ -660,24 +672,31 @@ __device__ void gemm1(const double* A22, int ldw, int s, const double* VT,
 // in registers for the whole row block; column tiles of 32 up to the
 // diagonal stream their C tile (HBM) and Bop rows (L2) through a kG2S-stage
 // cp.async pipeline in XOR-swizzled, unpadded shared memory, so two tiles
-// are in flight while one is computed.  Tiles crossing the diagonal also
+// are in flight while one is computed.  Bop fragments are 16-byte loads that
+// feed two DMMAs (adjacent k values per lane).  Tiles crossing the diagonal also
 // write their (never read) upper part.
 __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
-                      const double* V, double* sm) {
+                      const double* V, double* sm, int max_tiles = 1 << 30) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
   const int crow = 8 * warp + mm;  // this lane's row within the row block
   for (int rb = 0; rb < s; rb += kG2M) {
     const int r = rb + crow;
-    double af[kG2K / 4];
+    // k-pair q covers k = 8q .. 8q+7: lane kk takes k = 8q + 2kk in the
+    // first DMMA of the pair and 8q + 2kk + 1 in the second, so both operands
+    // of a pair are one 16-byte load
+    double2 af[kG2K / 8];
 #pragma unroll
-    for (int k4 = 0; k4 < kG2K / 4; ++k4) {
-      const int k = 4 * k4 + kk;
-      af[k4] = r < s ? -(k < kB ? W2[(long long)r * kB + k] : V[(long long)r * kB + k - kB])
-                     : 0.0;
+    for (int q = 0; q < kG2K / 8; ++q) {
+      const int k = 8 * q + 2 * kk;
+      double2 v = make_double2(0.0, 0.0);
+      if (r < s)
+        v = *reinterpret_cast<const double2*>(k < kB ? W2 + (long long)r * kB + k
+                                                     : V + (long long)r * kB + (k - kB));
+      af[q] = make_double2(-v.x, -v.y);
     }
     const int cend = min(rb + kG2M, s);
-    const int ncb = (cend + kG2N - 1) / kG2N;
+    const int ncb = min((cend + kG2N - 1) / kG2N, max_tiles);
     auto stage = [&](int ci) {
       if (ci < ncb) {
         const int cb = ci * kG2N;
@@ -688,7 +707,7 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
           const int bytes = gr < s ? 16 : 0;
           const long long g = (long long)(bytes ? gr : 0) * kB;
           const double* src = k2 < kB ? V + g + k2 : W2 + g + (k2 - kB);
-          cp_async16(st + row * kG2K + (k2 ^ (4 * (row & 3))), src, bytes);
+          cp_async16(st + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
         }
         double* cs = st + kG2N * kG2K;
         for (int t = tid; t < kG2M * (kG2N / 2); t += kNT) {
@@ -720,13 +739,17 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
         acc[nt][1] = x.y;
       }
 #pragma unroll
-      for (int k4 = 0; k4 < kG2K / 4; ++k4) {
-        const int kl = (4 * k4 + kk) ^ (4 * (mm & 3));
-        double bf[kG2N / 8];
+      for (int q = 0; q < kG2K / 8; ++q) {
+        const int kl = (8 * q + 2 * kk) ^ (8 * (mm & 1));
+        double2 bf[kG2N / 8];
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) bf[nt] = b[(8 * nt + mm) * kG2K + kl];
+        for (int nt = 0; nt < kG2N / 8; ++nt)
+          bf[nt] = *reinterpret_cast<const double2*>(b + (8 * nt + mm) * kG2K + kl);
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[k4], bf[nt]);
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
+          dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
+        }
       }
       if (r < s) {
         const int cb = ci * kG2N;
@@ -742,6 +765,201 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
       }
     }
     cpa_wait0();
+  }
+  __syncthreads();
+}
+
+// ---- fused: rest of panel p's update + SYMM of panel p+1 -----------------
+// A22n is the trailing matrix of panel p+1 (A22 of panel p without its first
+// kB rows and columns, whose update was applied beforehand).  One pass over
+// its lower tiles (64 x 32, row blocks in order, tiles up to the diagonal):
+//   C  = C - W2p Vp^T - Vp W2p^T            (panel p; written back)
+//   X[rb] += tril(C) VTn[cb]                 (registers, added per row block)
+//   X[cb] += strict(C)^T VTn[rb]             (read-modify-write per tile)
+// so the trailing matrix is read and written once per panel instead of being
+// read three times and written once.  Xn must be zero on entry; every X
+// element is accumulated in an order fixed by (n, panel), never by timing.
+// Shared memory: two stages of {Bop rows (swizzled), C tile (swizzled),
+// VTn[cb] rows} and the row block's VTn[rb] rows.
+__device__ __forceinline__ int cswz(int row, int col) {
+  return row * kG2N + (col ^ ((8 * (row & 1)) ^ (4 * ((row >> 1) & 1))));
+}
+
+__device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
+                           const double* Vp, const double* VTn, double* Xn,
+                           double* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = lane & 3, mm = lane >> 2;
+  const int crow = 8 * warp + mm;
+  double* sVr = sm + 2 * kFSt;
+  for (int rb = 0; rb < sn; rb += kG2M) {
+    const int r = rb + crow;
+    double2 af[kG2K / 8];
+#pragma unroll
+    for (int q = 0; q < kG2K / 8; ++q) {
+      const int k = 8 * q + 2 * kk;
+      double2 v = make_double2(0.0, 0.0);
+      if (r < sn)
+        v = *reinterpret_cast<const double2*>(k < kB ? W2p + (long long)r * kB + k
+                                                     : Vp + (long long)r * kB + (k - kB));
+      af[q] = make_double2(-v.x, -v.y);
+    }
+    double xr[kG2N / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < kG2N / 8; ++nt) xr[nt][0] = xr[nt][1] = 0.0;
+    const int cend = min(rb + kG2M, sn);
+    const int ncb = (cend + kG2N - 1) / kG2N;
+    auto stage = [&](int ci) {
+      if (ci < ncb) {
+        const int cb = ci * kG2N;
+        double* st = sm + (ci & 1) * kFSt;
+        for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
+          const int row = t >> 5, k2 = (t & 31) * 2;
+          const int gr = cb + row;
+          const int bytes = gr < sn ? 16 : 0;
+          const long long g = (long long)(bytes ? gr : 0) * kB;
+          const double* src = k2 < kB ? Vp + g + k2 : W2p + g + (k2 - kB);
+          cp_async16(st + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
+        }
+        double* cs = st + kG2N * kG2K;
+        for (int t = tid; t < kG2M * (kG2N / 2); t += kNT) {
+          const int row = t >> 4, c2 = (t & 15) * 2;
+          const int gr = rb + row, gc = cb + c2;
+          int bytes = 0;
+          if (gr < sn && gc < sn) bytes = gc + 1 < sn ? 16 : 8;
+          cp_async16(cs + cswz(row, c2), bytes ? A22n + (long long)gr * ldw + gc : A22n,
+                     bytes);
+        }
+        double* vc = cs + kG2M * kG2N;
+        for (int t = tid; t < kB * (kB / 2); t += kNT) {
+          const int row = t >> 4, c2 = (t & 15) * 2;
+          const int gr = cb + row;
+          const int bytes = gr < sn ? 16 : 0;
+          cp_async16(vc + row * kFVLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
+                     bytes);
+        }
+      }
+      cpa_commit();
+    };
+    __syncthreads();  // the previous row block is done with every buffer
+    for (int t = tid; t < kG2M * (kB / 2); t += kNT) {
+      const int row = t >> 4, c2 = (t & 15) * 2;
+      const int gr = rb + row;
+      const int bytes = gr < sn ? 16 : 0;
+      cp_async16(sVr + row * kFVRLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
+                 bytes);
+    }
+    stage(0);
+    for (int ci = 0; ci < ncb; ++ci) {
+      cpa_wait0();
+      __syncthreads();
+      stage(ci + 1);
+      const int cb = ci * kG2N;
+      const double* b = sm + (ci & 1) * kFSt;
+      double* cs = const_cast<double*>(b) + kG2N * kG2K;
+      const double* vc = cs + kG2M * kG2N;
+      // ---- rank-2kB update of this lane's C row
+      double acc[kG2N / 8][2];
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt) {
+        const double2 x = *reinterpret_cast<const double2*>(cs + cswz(crow, 8 * nt + 2 * kk));
+        acc[nt][0] = x.x;
+        acc[nt][1] = x.y;
+      }
+#pragma unroll
+      for (int q = 0; q < kG2K / 8; ++q) {
+        const int kl = (8 * q + 2 * kk) ^ (8 * (mm & 1));
+        double2 bf[kG2N / 8];
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt)
+          bf[nt] = *reinterpret_cast<const double2*>(b + (8 * nt + mm) * kG2K + kl);
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
+          dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt) {
+        const int col = cb + 8 * nt + 2 * kk;
+        if (r < sn) {
+          double* p = A22n + (long long)r * ldw + col;
+          if (col + 1 < sn)
+            *reinterpret_cast<double2*>(p) = make_double2(acc[nt][0], acc[nt][1]);
+          else if (col < sn)
+            p[0] = acc[nt][0];
+        }
+        *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
+            make_double2(acc[nt][0], acc[nt][1]);
+      }
+      __syncthreads();
+      const bool diag = cb + kB > rb;  // the tile may cross the diagonal
+      // ---- X[rb] += tril(C) VTn[cb]   (this lane's row, k = tile columns)
+#pragma unroll
+      for (int q = 0; q < kB / 8; ++q) {
+        const int k = 8 * q + 2 * kk;
+        double2 a = *reinterpret_cast<const double2*>(cs + cswz(crow, k));
+        if (diag && cb + k > r) a.x = 0.0;
+        if (diag && cb + k + 1 > r) a.y = 0.0;
+        double b0[kG2N / 8], b1[kG2N / 8];
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          b0[nt] = vc[k * kFVLD + 8 * nt + mm];
+          b1[nt] = vc[(k + 1) * kFVLD + 8 * nt + mm];
+        }
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          dmma(xr[nt][0], xr[nt][1], a.x, b0[nt]);
+          dmma(xr[nt][0], xr[nt][1], a.y, b1[nt]);
+        }
+      }
+      // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 16 cols)
+      {
+        const int mt2 = warp >> 1, nb = 2 * (warp & 1);
+        const int xrow = cb + 8 * mt2 + mm;
+        double x2[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int xc = 8 * (nb + u) + 2 * kk;
+          if (xrow < sn) {
+            const double2 t = *reinterpret_cast<const double2*>(Xn + (long long)xrow * kB + xc);
+            x2[u][0] = t.x;
+            x2[u][1] = t.y;
+          } else {
+            x2[u][0] = x2[u][1] = 0.0;
+          }
+        }
+        const int ccol = 8 * mt2 + mm;  // tile column of C = X row
+#pragma unroll 4
+        for (int k4 = 0; k4 < kG2M / 4; ++k4) {
+          const int krow = 4 * k4 + kk;  // tile row of C = contraction index
+          const double v = cs[cswz(krow, ccol)];
+          const double a = (diag && rb + krow <= cb + ccol) ? 0.0 : v;
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            dmma(x2[u][0], x2[u][1], a, sVr[krow * kFVRLD + 8 * (nb + u) + mm]);
+        }
+        if (xrow < sn) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            *reinterpret_cast<double2*>(Xn + (long long)xrow * kB + 8 * (nb + u) + 2 * kk) =
+                make_double2(x2[u][0], x2[u][1]);
+        }
+      }
+    }
+    // X[rb] += the row-part accumulators (after this row block's transposed
+    // contributions to the same rows)
+    __syncthreads();
+    if (r < sn) {
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt) {
+        double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + 8 * nt + 2 * kk);
+        double2 x = *p;
+        x.x += xr[nt][0];
+        x.y += xr[nt][1];
+        *p = x;
+      }
+    }
   }
   __syncthreads();
 }
@@ -767,7 +985,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                    \
     __syncthreads();                                                      \
     const long long now_ = clock64();                                     \
-    if (threadIdx.x == 0 && blockIdx.x == 0)                              \
+    if (threadIdx.x == 0)                              \
       atomicAdd(&g_phase_cycles[ph_], (unsigned long long)(now_ - t_ph_)); \
     t_ph_ = now_;                                                         \
     ph_ = (id);                                                           \
@@ -804,10 +1022,13 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
   int* sflag = reinterpret_cast<int*>(sS + kB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = args.n, ldw = args.ldw;
+  // slot workspace: the minor (n x ldw), then V and X (= W2) for two panels
+  // and VT, n x kB each (stage1_ws_doubles)
   double* W = args.ws + blockIdx.x * args.ws_stride;
-  double* Vg = W + (long long)n * ldw;
-  double* VTg = Vg + (long long)n * kB;
-  double* Xg = VTg + (long long)n * kB;
+  double* const Vg[2] = {W + (long long)n * ldw, W + (long long)n * ldw + (long long)n * kB};
+  double* const Xg[2] = {W + (long long)n * ldw + 2LL * n * kB,
+                         W + (long long)n * ldw + 3LL * n * kB};
+  double* VTg = W + (long long)n * ldw + 4LL * n * kB;
 
   // Solves are pulled from a work queue: the two CTAs sharing an SM do not
   // progress at the same rate, so a static blockIdx stride leaves one of
@@ -841,24 +1062,22 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
       }
     }
     __syncthreads();
-    int c = 0;
-    for (; c < m; c += kB) {
-      const int s = m - c - kB;
-      if (s < 2) break;
-      const int c0 = c + kB;
-      double* P0 = W + (long long)c0 * ldw + c;
+    // Panel factorisation of columns c..c+kB-1 (trailing size s): V (Vb),
+    // T (sT), the band columns, VT = V T; Xb is scratch.
+    auto factor = [&](int c, int s, double* Vb, double* Xb) {
+      double* P0 = W + (long long)(c + kB) * ldw + c;
       PHASE(2);
       const bool fast = s >= 2 * kB &&
-                        chol_panel(P0, ldw, s, Vg, Xg, sT, sG, sA, sB, sR, sS,
+                        chol_panel(P0, ldw, s, Vb, Xb, sT, sG, sA, sB, sR, sS,
                                    sgemm, sflag);
       if (!fast) {
 #ifdef EIGENID_PHASE_TIMING
-        if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_phase_cycles[15], 1ull);
+        if (tid == 0) atomicAdd(&g_phase_cycles[15], 1ull);
 #endif
         panel_qr(P0, ldw, s, stau, red, wsm);
-        extract_v(P0, ldw, s, Vg);
+        extract_v(P0, ldw, s, Vb);
         // T (dlarft, forward columnwise) from G = V^T V
-        gram(Vg, kB, Vg, kB, s, sG, sgemm);
+        gram(Vb, kB, Vb, kB, s, sG, sgemm);
         if (warp == 0) {
           for (int t = 0; t < kB; ++t) {
             double v = 0.0;
@@ -875,12 +1094,12 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
       __syncthreads();
       PHASE(3);
       write_band(W, ldw, m, c, c + kB, band);
-      row_transform(Vg, kB, sT, 1.0, nullptr, VTg, s);       // VT = V T
-      double* A22 = W + (long long)c0 * ldw + c0;
-      PHASE(4);
-      gemm1(A22, ldw, s, VTg, Xg, sgemm);                     // X = A22 VT
+      row_transform(Vb, kB, sT, 1.0, nullptr, VTg, s);        // VT = V T
+    };
+    // W2 = X - V M/2 with M = T^T (V^T X), in place in Xb.
+    auto form_w2 = [&](int s, const double* Vb, double* Xb) {
       PHASE(5);
-      gram(Vg, kB, Xg, kB, s, sG, sgemm);                     // Y = V^T X
+      gram(Vb, kB, Xb, kB, s, sG, sgemm);                     // Y = V^T X
       for (int t = tid; t < kB * kB; t += kNT) {              // M = T^T Y
         const int q = t / kB, p = t % kB;
         double v = 0.0;
@@ -888,11 +1107,57 @@ __global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
         sM[q * kSmallLD + p] = v;
       }
       __syncthreads();
-      row_transform(Vg, kB, sM, -0.5, Xg, Xg, s);             // W2 = X - V M/2
+      row_transform(Vb, kB, sM, -0.5, Xb, Xb, s);
+    };
+    int c = 0;
+#if EIGENID_STAGE1_FUSED
+    // Look-ahead schedule: panel p+1's columns are updated and factored
+    // first, then one fused pass applies the rest of panel p's update and
+    // forms X of panel p+1 (gemm_fused).
+    if (m - kB >= 2) {
+      int par = 0;
+      factor(0, m - kB, Vg[0], Xg[0]);
+      PHASE(4);
+      gemm1(W + (long long)kB * ldw + kB, ldw, m - kB, VTg, Xg[0], sgemm);
+      form_w2(m - kB, Vg[0], Xg[0]);
+      for (;;) {
+        const int s = m - c - kB;
+        double* A22 = W + (long long)(c + kB) * ldw + (c + kB);
+        const int s1 = s - kB;
+        PHASE(6);
+        if (s1 < 2) {
+          gemm2(A22, ldw, s, Xg[par], Vg[par], sgemm);         // last update
+          PHASE(7);
+          c += kB;
+          break;
+        }
+        gemm2(A22, ldw, s, Xg[par], Vg[par], sgemm, 1);        // next panel's columns
+        const int nxt = par ^ 1;
+        factor(c + kB, s1, Vg[nxt], Xg[nxt]);
+        for (int t = tid; t < s1 * kB; t += kNT) Xg[nxt][t] = 0.0;
+        __syncthreads();
+        PHASE(4);
+        gemm_fused(A22 + (long long)kB * ldw + kB, ldw, s1, Xg[par] + kB * kB,
+                   Vg[par] + kB * kB, VTg, Xg[nxt], sgemm);
+        form_w2(s1, Vg[nxt], Xg[nxt]);
+        c += kB;
+        par = nxt;
+      }
+    }
+#else
+    for (; c < m; c += kB) {
+      const int s = m - c - kB;
+      if (s < 2) break;
+      factor(c, s, Vg[0], Xg[0]);
+      double* A22 = W + (long long)(c + kB) * ldw + (c + kB);
+      PHASE(4);
+      gemm1(A22, ldw, s, VTg, Xg[0], sgemm);                   // X = A22 VT
+      form_w2(s, Vg[0], Xg[0]);
       PHASE(6);
-      gemm2(A22, ldw, s, Xg, Vg, sgemm);                      // A22 -= W2V^T+VW2^T
+      gemm2(A22, ldw, s, Xg[0], Vg[0], sgemm);                 // A22 -= W2V^T+VW2^T
       PHASE(7);
     }
+#endif
     write_band(W, ldw, m, c, m, band);
     __syncthreads();
   }
@@ -914,6 +1179,9 @@ extern "C" void eigenid_debug_cta_span(unsigned long long* out) {
 size_t stage1_smem_bytes() { return sizeof(double) * (size_t)kStage1SmemDoubles; }
 int stage1_band_ld() { return kLDAB; }
 int stage1_bandwidth() { return kB; }
+long long stage1_ws_doubles(int n, int ldw) {
+  return (long long)n * ldw + 5LL * n * kB;
+}
 
 cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st) {
   const size_t smem = stage1_smem_bytes();

@@ -20,13 +20,14 @@ buf = (ctypes.c_ulonglong * 16)()
 lib.eigenid_debug_phase_cycles(buf)
 names = ['other', 'copy', 'panel', 'band+VT', 'gemm1', 'Y,M,W2', 'gemm2', '-']
 tot = sum(buf[i] for i in range(8))
-print('stage 1 (CTA 0):')
-for i in range(8): print(f'  {names[i]:10s} {buf[i]/1.965e9*1e3:9.2f} ms  {100*buf[i]/max(tot,1):5.1f}%')
+g1 = min(rows + 1, 296)
+print(f'stage 1 (summed over {g1} CTAs, shown per CTA):')
+for i in range(8): print(f'  {names[i]:10s} {buf[i]/g1/1.965e9*1e3:9.2f} ms  {100*buf[i]/max(tot,1):5.1f}%')
 names2 = ['gram P', 'chol+inv', 'row_transform x3', 'gram Q', 'check+chol+mul+inv', '-', 'LU+inv+T+V']
 print('  chol_panel sub-phases:')
 for i in range(7):
-    if names2[i] != '-': print(f'    {names2[i]:20s} {buf[8+i]/1.965e9*1e3:9.2f} ms')
-print(f'  panel_qr fallbacks (CTA 0): {buf[15]}')
+    if names2[i] != '-': print(f'    {names2[i]:20s} {buf[8+i]/g1/1.965e9*1e3:9.2f} ms')
+print(f'  panel_qr fallbacks (all CTAs): {buf[15]}')
 sp = (ctypes.c_ulonglong * 1536)()
 lib.eigenid_debug_cta_span(sp)
 g = min(rows + 1, 296)
