@@ -858,6 +858,25 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       const double* b = sm + (ci & 1) * kFSt;
       double* cs = const_cast<double*>(b) + kG2N * kG2K;
       const double* vc = cs + kG2M * kG2N;
+      // X[cb] block of this warp for the transposed product below, loaded
+      // early so the read overlaps the rank-2kB update
+      const int mt2 = warp >> 1, nb = 2 * (warp & 1);
+      const int xrow = cb + 8 * mt2 + mm;
+      double x2[2][2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int xc = 8 * (nb + u) + 2 * kk;
+        if (xrow < sn) {
+          double2 t;
+          asm volatile("ld.global.v2.f64 {%0, %1}, [%2];\n"
+                       : "=d"(t.x), "=d"(t.y)
+                       : "l"(Xn + (long long)xrow * kB + xc));
+          x2[u][0] = t.x;
+          x2[u][1] = t.y;
+        } else {
+          x2[u][0] = x2[u][1] = 0.0;
+        }
+      }
       // ---- rank-2kB update of this lane's C row
       double acc[kG2N / 8][2];
 #pragma unroll
@@ -915,20 +934,6 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       }
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 16 cols)
       {
-        const int mt2 = warp >> 1, nb = 2 * (warp & 1);
-        const int xrow = cb + 8 * mt2 + mm;
-        double x2[2][2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int xc = 8 * (nb + u) + 2 * kk;
-          if (xrow < sn) {
-            const double2 t = *reinterpret_cast<const double2*>(Xn + (long long)xrow * kB + xc);
-            x2[u][0] = t.x;
-            x2[u][1] = t.y;
-          } else {
-            x2[u][0] = x2[u][1] = 0.0;
-          }
-        }
         const int ccol = 8 * mt2 + mm;  // tile column of C = X row
 #pragma unroll 4
         for (int k4 = 0; k4 < kG2M / 4; ++k4) {
