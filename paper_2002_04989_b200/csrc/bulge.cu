@@ -58,6 +58,39 @@ __device__ __forceinline__ void st_pred(double* p, double v, bool pred) {
 __device__ __forceinline__ void cpa_commit2() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cpa_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
+// Full-block (L = kCB) variants with immediate address offsets: element c of
+// a column run lives kCLD-1 doubles further on, so every load/store is one
+// instruction off a single base register (no per-element address or
+// predicate arithmetic beyond the triangle test).
+template <int C>
+__device__ __forceinline__ void st_tri_full(double* base, const double (&v)[kCB], int lane) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ge.s32 q, %2, %3;\n @q st.global.f64 [%0+%4], %1;\n}\n" ::"l"(base),
+      "d"(v[C]), "r"(lane), "n"(C), "n"(C * (kCLD - 1) * 8)
+      : "memory");
+  if constexpr (C + 1 < kCB) st_tri_full<C + 1>(base, v, lane);
+}
+template <int C>
+__device__ __forceinline__ void st_full(double* base, const double (&v)[kCB]) {
+  asm volatile("st.global.f64 [%0+%2], %1;\n" ::"l"(base), "d"(v[C]), "n"(C * (kCLD - 1) * 8)
+               : "memory");
+  if constexpr (C + 1 < kCB) st_full<C + 1>(base, v);
+}
+template <int C>
+__device__ __forceinline__ void cpa_tri_full(unsigned sbase, const double* gbase, int lane) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ge.s32 q, %2, %3;\n @q cp.async.ca.shared.global [%0+%4], [%1+%5], 8;\n}\n" ::"r"(
+          sbase),
+      "l"(gbase), "r"(lane), "n"(C), "n"(C * 8), "n"(C * (kCLD - 1) * 8));
+  if constexpr (C + 1 < kCB) cpa_tri_full<C + 1>(sbase, gbase, lane);
+}
+template <int C>
+__device__ __forceinline__ void cpa_full(unsigned sbase, const double* gbase) {
+  asm volatile("cp.async.ca.shared.global [%0+%2], [%1+%3], 8;\n" ::"r"(sbase), "l"(gbase),
+               "n"(C * 8), "n"(C * (kCLD - 1) * 8));
+  if constexpr (C + 1 < kCB) cpa_full<C + 1>(sbase, gbase);
+}
+
 
 // Householder from x (lane r holds x_r, r < L): v (v_0 = 1) -> sv, returns
 // tau, *beta.  dlarfg convention.
@@ -85,6 +118,7 @@ __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
 // D <- H D H on the L x L diagonal block whose lower triangle is held in sD
 // (filled by cp.async; rows/cols >= L are zero; the upper triangle is read
 // through the mirror).  Writes the lower triangle back to the band.
+template <bool FULL>
 __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
                                                 double tau, double* sw, int L,
                                                 double* AB, int R) {
@@ -116,9 +150,13 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
   }
   // lower triangle back to the band: column c, rows c..L-1 (coalesced in r)
   double* base = AB + (long long)R * kCLD + lane;
+  if constexpr (FULL) {
+    st_tri_full<0>(base, drow, lane);
+  } else {
 #pragma unroll
-  for (int c = 0; c < kCB; ++c)
-    st_pred(base + c * (kCLD - 1), drow[c], lane >= c && lane < L);
+    for (int c = 0; c < kCB; ++c)
+      st_pred(base + c * (kCLD - 1), drow[c], lane >= c && lane < L);
+  }
   __syncwarp();
 }
 
@@ -129,6 +167,11 @@ __device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
   // out-of-range entries are zero-filled
   const int lane = threadIdx.x & 31;
   const double* base = AB + (long long)R * kCLD + lane;
+  if (L == kCB) {
+    cpa_tri_full<0>((unsigned)__cvta_generic_to_shared(sD + dp(lane, 0)), base, lane);
+    cpa_commit2();
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < kCB; ++c) {
     if (lane >= c) {
@@ -145,6 +188,11 @@ __device__ __forceinline__ void prefetch_c(double* sC, const double* AB, int R1,
                                            int L1, int R, int L) {
   const int lane = threadIdx.x & 31;
   const double* base = AB + (long long)R * kCLD + (R1 - R) + lane;
+  if (L1 == kCB && L == kCB) {
+    cpa_full<0>((unsigned)__cvta_generic_to_shared(sC + lane * kSLD), base);
+    cpa_commit2();
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < kCB; ++c) {
     const bool ok = lane < L1 && c < L;
@@ -236,7 +284,10 @@ bulge_chase_kernel(Stage2Args a) {
       if (lane < L0) AB[(long long)st * kCLD + 1 + lane] = (lane == 0) ? beta : 0.0;
       cpa_wait_all();
       __syncwarp();
-      two_sided_store(sD0, sv, tau, sw, L0, AB, R0);
+      if (L0 == kCB)
+        two_sided_store<true>(sD0, sv, tau, sw, L0, AB, R0);
+      else
+        two_sided_store<false>(sD0, sv, tau, sw, L0, AB, R0);
       publish(prog, warp, st, 0);
       int R = R0, L = L0, buf = 1, k = 1;
       while (have) {
@@ -308,15 +359,23 @@ bulge_chase_kernel(Stage2Args a) {
             crow[2 * h + 1] -= vr * a.y;
           }
         }
+        const bool full = Lk == kCB && L == kCB;
         {
           double* base = AB + (long long)R * kCLD + (Rk - R) + lane;
+          if (full) {
+            st_full<0>(base, crow);
+          } else {
 #pragma unroll
-          for (int c = 0; c < kCB; ++c)
-            st_pred(base + c * (kCLD - 1), crow[c], lane < Lk && c < L);
+            for (int c = 0; c < kCB; ++c)
+              st_pred(base + c * (kCLD - 1), crow[c], lane < Lk && c < L);
+          }
         }
         BPH(3);
         BPH(4);
-        two_sided_store(sD0 + buf * kDP, sv2, tau2, sw, Lk, AB, Rk);
+        if (Lk == kCB)
+          two_sided_store<true>(sD0 + buf * kDP, sv2, tau2, sw, Lk, AB, Rk);
+        else
+          two_sided_store<false>(sD0 + buf * kDP, sv2, tau2, sw, Lk, AB, Rk);
         BPH(5);
         sv[lane] = sv2[lane];
         publish(prog, warp, st, k);
