@@ -70,27 +70,124 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
   double* out = a.out + (long long)(solve - a.first_solve) * a.out_ld;
   const int per = (m + a.split - 1) / a.split;
   const int k0 = part * per, k1 = min(m, k0 + per);
-  for (int k = k0 + threadIdx.x; k < k1; k += kBisNT) {
-    double res = 0.0;
-    bool done = false;
+  // Each thread owns eigenvalues k = k0 + tid, + kBisNT, ... and runs them as
+  // a state machine, one Sturm evaluation per round: bracket low end, high
+  // end, then safeguarded secant/bisection (the arithmetic of bisect_from).
+  // A lane whose eigenvalue converges starts its next one in the same round,
+  // so the warp's rounds follow the mean, not the maximum, evaluation count.
+  // The interlacing bracket (minors) is verified by the counts at both ends;
+  // if either check fails the lane restarts on the Gershgorin interval.
+  const double glo_s = glo * sc, ghi_s = ghi * sc;
+  int k = k0 + threadIdx.x;
+  bool active = k < k1;
+  bool gersh = false;
+  int stage = 0, it = 0, side = 0, clo = 0, chi = 0, elo = 0, ehi = 0;
+  double lo = 0.0, hi = 0.0, plo = 0.0, phi = 0.0, w1 = 0.0, w2 = 0.0;
+  auto start = [&]() {
+    stage = 0;
     if (a.lam) {
-      // interlacing bracket, verified by the Sturm counts at both ends; the
-      // end evaluations seed the secant iteration
-      const double l0 = fmax(a.lam[k] - delta, glo), l1 = fmin(a.lam[k + 1] + delta, ghi);
-      double p0, p1;
-      int e0, e1;
-      const int c0 = sturm_det(sd, se2, m, l0 * sc, &p0, &e0);
-      if (c0 <= k && l0 < l1) {
-        const int c1 = sturm_det(sd, se2, m, l1 * sc, &p1, &e1);
-        if (c1 > k) {
-          res = bisect_from(sd, se2, m, k, l0 * sc, l1 * sc, atol, c0, p0, e0,
-                            c1, p1, e1);
-          done = true;
+      gersh = false;
+      lo = fmax(a.lam[k] - delta, glo) * sc;
+      hi = fmin(a.lam[k + 1] + delta, ghi) * sc;
+    } else {
+      gersh = true;
+      lo = glo_s;
+      hi = ghi_s;
+    }
+  };
+  if (active) start();
+  while (__any_sync(0xffffffffu, active)) {
+    double x = 0.0;
+    if (active) {
+      if (stage == 2) {
+        bool fin = false;
+        const double w = hi - lo;
+        const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
+        if (w <= tol || it >= 300) {
+          fin = true;
+        } else {
+          x = lo + 0.5 * w;
+          const bool slow = it >= 2 && w > 0.5 * w2;
+          if (clo == k && chi == k + 1 && !slow) {
+            const int de = ehi - elo;
+            double r = phi / plo;
+            r = de > 1000 ? -1e300 : (de < -1000 ? -1e-300 : scalbn(r, de));
+            const double xs = lo + w / (1.0 - r);
+            const double g = 0.5 * tol;
+            x = fmin(fmax(xs, lo + g), hi - g);
+            if (!(x > lo && x < hi)) x = lo + 0.5 * w;
+          } else {
+            side = 0;
+          }
+          w2 = w1;
+          w1 = w;
+          if (!(x > lo && x < hi)) fin = true;  // a few ulps wide
         }
+        if (fin) {
+#ifdef EIGENID_BISECT_STATS
+          atomicAdd(&g_bis_hist[it < 63 ? it : 63], 1ull);
+#endif
+          out[k] = (lo + 0.5 * (hi - lo)) / sc;
+          k += kBisNT;
+          active = k < k1;
+          if (active) {
+            start();
+            x = lo;
+          }
+        }
+      } else {
+        x = stage == 0 ? lo : hi;
       }
     }
-    if (!done) res = bisect_one(sd, se2, m, k, glo * sc, ghi * sc, atol);
-    out[k] = res / sc;
+    if (active) {
+      double px;
+      int ex;
+      const int cx = sturm_det(sd, se2, m, x, &px, &ex);
+      if (stage == 0) {
+        clo = cx;
+        plo = px;
+        elo = ex;
+        if (!gersh && !(cx <= k && lo < hi)) {
+          gersh = true;  // interlacing check failed: Gershgorin bracket
+          lo = glo_s;
+          hi = ghi_s;
+        } else {
+          stage = 1;
+        }
+      } else if (stage == 1) {
+        chi = cx;
+        phi = px;
+        ehi = ex;
+        if (!gersh && !(cx > k)) {
+          gersh = true;
+          lo = glo_s;
+          hi = ghi_s;
+          stage = 0;
+        } else {
+          stage = 2;
+          it = 0;
+          side = 0;
+          w1 = w2 = 0.0;
+        }
+      } else {
+        if (cx > k) {
+          hi = x;
+          phi = px;
+          ehi = ex;
+          chi = cx;
+          if (side == 1) plo *= 0.5;  // Illinois: retained end twice
+          side = 1;
+        } else {
+          lo = x;
+          plo = px;
+          elo = ex;
+          clo = cx;
+          if (side == -1) phi *= 0.5;
+          side = -1;
+        }
+        ++it;
+      }
+    }
   }
   if (a.split > 1) return;  // cross-CTA order is checked by sort_fix_kernel
   __syncthreads();
@@ -149,5 +246,11 @@ cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
   }
   return cudaGetLastError();
 }
+
+#ifdef EIGENID_BISECT_STATS
+extern "C" void eigenid_debug_bisect_hist(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_bis_hist, sizeof(g_bis_hist));
+}
+#endif
 
 }  // namespace eigenid_b200

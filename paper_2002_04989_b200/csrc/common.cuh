@@ -130,11 +130,16 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d,
 // Eigenvalue k (0-based, ascending) of the scaled (d, e2) inside [lo, hi)
 // with count(lo) <= k < count(hi).  Bisection until the bracket isolates
 // eigenvalue k (count(lo) == k, count(hi) == k+1), then Illinois-modified
-// regula falsi on det(T - x), which has exactly one sign change there; every
-// trial point still updates the bracket by its Sturm count, so the result is
-// the same eigenvalue bisection would find.  Stops at
+// regula falsi on det(T - x), which has exactly one sign change there, with
+// Brent-style safeguards (bisect when two steps did not halve the bracket;
+// trial points at least half a tolerance inside); every trial point still
+// updates the bracket by its Sturm count, so the result is the same
+// eigenvalue bisection would find.  Stops at
 // hi - lo <= max(atol, 2 eps max(|lo|,|hi|)) — the accuracy the
 // Householder reduction's backward error (~eps ||T||) supports.
+#ifdef EIGENID_BISECT_STATS
+static __device__ unsigned long long g_bis_hist[64];  // evaluations per eigenvalue
+#endif
 __device__ __forceinline__ double bisect_from(const double* __restrict__ d,
                                               const double* __restrict__ e2,
                                               int m, int k, double lo,
@@ -142,24 +147,31 @@ __device__ __forceinline__ double bisect_from(const double* __restrict__ d,
                                               double plo, int elo, int chi,
                                               double phi, int ehi) {
   int side = 0;
-  for (int it = 0; it < 300; ++it) {
+  int it = 0;
+  double w1 = 0.0, w2 = 0.0;  // bracket widths one and two steps ago
+  for (; it < 300; ++it) {
     const double w = hi - lo;
     const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
     if (w <= tol) break;
     double x = lo + 0.5 * w;
-    // secant step when eigenvalue k is isolated; every third step bisects
-    // (safeguard), and secant points are kept 1% inside the bracket
-    if (clo == k && chi == k + 1 && it % 3 != 2) {
+    // secant (Illinois) step once eigenvalue k is isolated, unless the last
+    // two steps did not halve the bracket; the trial point keeps half a
+    // tolerance from both ends, so a converged secant estimate is bracketed
+    // within one tolerance by the next one or two evaluations
+    const bool slow = it >= 2 && w > 0.5 * w2;
+    if (clo == k && chi == k + 1 && !slow) {
       const int de = ehi - elo;
       double r = phi / plo;
       r = de > 1000 ? -1e300 : (de < -1000 ? -1e-300 : scalbn(r, de));
       const double xs = lo + w / (1.0 - r);
-      const double g = 0.01 * w;
+      const double g = 0.5 * tol;
       x = fmin(fmax(xs, lo + g), hi - g);
       if (!(x > lo && x < hi)) x = lo + 0.5 * w;
     } else {
       side = 0;
     }
+    w2 = w1;
+    w1 = w;
     if (!(x > lo && x < hi)) break;  // interval is a few ulps wide
     double px;
     int ex;
@@ -180,6 +192,9 @@ __device__ __forceinline__ double bisect_from(const double* __restrict__ d,
       side = -1;
     }
   }
+#ifdef EIGENID_BISECT_STATS
+  atomicAdd(&g_bis_hist[it < 63 ? it : 63], 1ull);
+#endif
   return lo + 0.5 * (hi - lo);
 }
 
