@@ -20,8 +20,9 @@
 // warps measured slower: 168 registers per thread and a smaller L1).  Within
 // a sweep a step never reads what the previous step wrote, so the blocks of
 // step k+1 are prefetched by cp.async while step k computes: the lower
-// triangle of D (packed) into a double buffer, C into the transposition
-// buffer once step k's left-apply has consumed it.
+// triangle of D (packed) into a double buffer, C into sC as soon as step k
+// has read its rows (the left-apply's column sums are a shuffle butterfly,
+// not a shared-memory transpose).
 // CTAs pull solves from an atomic work counter (persistent kernel).
 #include "kernels.cuh"
 
@@ -306,6 +307,8 @@ bulge_chase_kernel(Stage2Args a) {
           wait_prev(prog, warp, st, k + 2);
           BPH(6);
           prefetch_d(sD0 + (buf ^ 1) * kDP, AB, Rn, Ln);
+          __syncwarp();  // every lane has read its C row from sC
+          prefetch_c(sC, AB, Rn, Ln, Rk, Lk);
         }
         BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
@@ -329,26 +332,33 @@ bulge_chase_kernel(Stage2Args a) {
         const double tau2 = warp_householder(crow[0], Lk, sv2, &beta2);
         crow[0] = (lane == 0) ? beta2 : 0.0;
         BPH(2);
-        // left-apply to columns 1..L-1: w_c = sum_r v2_r C[r][c]
-#pragma unroll
-        for (int c = 0; c < kCB; ++c) sC[lane * kSLD + c] = crow[c];
-        __syncwarp();
+        // left-apply to columns 1..L-1: w_c = tau2 sum_r v2_r C[r][c], the
+        // column sums by a butterfly reduce-scatter over the lanes (after
+        // round o, a lane holds partial sums for the half of its columns
+        // selected by lane bit o; lane c ends with column c)
         {
-          const double2* u2 = reinterpret_cast<const double2*>(sv2);
-          double ww[4] = {0.0, 0.0, 0.0, 0.0};
+          const double vr2 = sv2[lane];
+          double ps[kCB / 2];
 #pragma unroll
-          for (int h = 0; h < kCB / 2; ++h) {
-            const double2 u = u2[h];
-            ww[(2 * h) & 3] += u.x * sC[(2 * h) * kSLD + lane];
-            ww[(2 * h + 1) & 3] += u.y * sC[(2 * h + 1) * kSLD + lane];
+          for (int j = 0; j < kCB / 2; ++j) {
+            const bool up = lane & 16;
+            const double send = vr2 * (up ? crow[j] : crow[j + 16]);
+            const double keep = vr2 * (up ? crow[j + 16] : crow[j]);
+            ps[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
           }
-          const double w = (ww[0] + ww[1]) + (ww[2] + ww[3]);
-          sw[lane] = (lane >= 1 && lane < L) ? tau2 * w : 0.0;
+#pragma unroll
+          for (int o = 8; o >= 1; o >>= 1) {
+#pragma unroll
+            for (int j = 0; j < o; ++j) {
+              const bool up = lane & o;
+              const double send = up ? ps[j] : ps[j + o];
+              const double keep = up ? ps[j + o] : ps[j];
+              ps[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          sw[lane] = (lane >= 1 && lane < L) ? tau2 * ps[0] : 0.0;
         }
         __syncwarp();
-        // sC is free again: next step's C block lands during the two-sided
-        // update below
-        if (haven) prefetch_c(sC, AB, Rn, Ln, Rk, Lk);
         {
           const double vr = sv2[lane];
           const double2* w2 = reinterpret_cast<const double2*>(sw);
