@@ -745,11 +745,12 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt)
           bf[nt] = *reinterpret_cast<const double2*>(b + (8 * nt + mm) * kG2K + kl);
+        // independent accumulators back to back (the DMMAs are volatile, so
+        // this order is the issue order)
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) {
-          dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
-          dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
-        }
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
       }
       if (r < s) {
         const int cb = ci * kG2N;
@@ -892,11 +893,12 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt)
           bf[nt] = *reinterpret_cast<const double2*>(b + (8 * nt + mm) * kG2K + kl);
+        // independent accumulators back to back (the DMMAs are volatile, so
+        // this order is the issue order)
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) {
-          dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
-          dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
-        }
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
       }
 #pragma unroll
       for (int nt = 0; nt < kG2N / 8; ++nt) {
@@ -927,10 +929,9 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           b1[nt] = vc[(k + 1) * kFVLD + 8 * nt + mm];
         }
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) {
-          dmma(xr[nt][0], xr[nt][1], a.x, b0[nt]);
-          dmma(xr[nt][0], xr[nt][1], a.y, b1[nt]);
-        }
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], a.x, b0[nt]);
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], a.y, b1[nt]);
       }
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 16 cols)
       {
