@@ -60,7 +60,6 @@ namespace {
 
 constexpr int kSmallMax = 64;
 constexpr int kLargeMax = 14000;  // bisection stages (d, e^2) in shared memory
-constexpr int kStage1Slots = 296;  // two band-reduction CTAs per SM
 
 struct DevBuf {
   void* p = nullptr;
@@ -261,7 +260,10 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   }
   const double ws_bytes = 8.0 * ws_stride;
   const double solve_bytes = 8.0 * (band_stride + 3.0 * n);
-  int slots = nsolves < kStage1Slots ? nsolves : kStage1Slots;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int max_slots = sms * stage1_ctas_per_sm();
+  int slots = nsolves < max_slots ? nsolves : max_slots;
   while (slots > 1 && slots * ws_bytes > 0.7 * budget) slots = (slots + 1) / 2;
   long long chunk = (long long)((budget - slots * ws_bytes) / solve_bytes);
   if (chunk > nsolves) chunk = nsolves;

@@ -22,32 +22,42 @@
 namespace eigenid_b200 {
 
 constexpr int kB = 32;      // bandwidth / panel width
-constexpr int kNT = 256;    // threads per CTA (8 warps)
+// Two layouts: 8 warps and two CTAs per SM (64-row GEMM blocks), or "wide":
+// 16 warps and one CTA per SM (128-row blocks: half the operand re-reads
+// per trailing element, three-stage fused pipeline).
+#ifndef EIGENID_STAGE1_WIDE
+#define EIGENID_STAGE1_WIDE 0
+#endif
+constexpr int kNT = EIGENID_STAGE1_WIDE ? 512 : 256;  // threads per CTA
+constexpr int kNW = kNT / 32;                         // warps per CTA
+constexpr int kCtasPerSm = EIGENID_STAGE1_WIDE ? 1 : 2;
 constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
-// Shared-memory layout (doubles).  Two CTAs (8 warps each) per SM; the GEMM
-// region is reused by the panel / Gram phases.
-constexpr int kG2M = 64, kG2N = 32, kG2K = 2 * kB;  // GEMM2 row block / tile / k
+// Shared-memory layout (doubles); the GEMM region is reused by the panel /
+// Gram phases.  Every warp owns 8 rows of a GEMM-2 / fused row block.
+constexpr int kG2M = 8 * kNW, kG2N = 32, kG2K = 2 * kB;  // row block / tile / k
 constexpr int kG1M = 64, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 68;
-constexpr int kMT1 = kG1M / 32;                     // 8-row m-tiles per warp
+constexpr int kMT1 = 8 * kG1M / kNT;                // 8-row m-tiles per warp
 constexpr int kG1_A = kG1M * kG1LDA;                // pass 1: A chunk 128 x 32
 constexpr int kG1_T = kG1K * kG1TLD;                // pass 2: A chunk 32 x 128
 constexpr int kG1_B = kG1K * kG1LDB;                // VT chunk 32 x 32
 constexpr int kSmallLD = kB + 1;
 constexpr int kSmallMat = kB * kSmallLD;            // T, G/Y, M
-constexpr int kGramPart = 8 * kSmallMat;
+constexpr int kGramPart = 8 * kSmallMat;             // 8 partial Gram slots
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int kG1S = 3;                             // GEMM 1 cp.async stages
 constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
+constexpr int kFS = EIGENID_STAGE1_WIDE ? 3 : 2;      // fused-pass stages
+constexpr int kXT = 16 / kNW;  // 8x8 tiles of the fused transposed product per warp
 constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
 #ifndef EIGENID_STAGE1_FUSED
 #define EIGENID_STAGE1_FUSED 1
 #endif
-// Fused pass (rest of panel p's update + SYMM of panel p+1): two stages of
+// Fused pass (rest of panel p's update + SYMM of panel p+1): kFS stages of
 // {Bop rows, C tile, VT(cb) rows} plus the row block's VT(rb) rows.
 constexpr int kFVLD = 34, kFVRLD = 36;
 constexpr int kFSt = kG2N * kG2K + kG2M * kG2N + kB * kFVLD;
-constexpr int kFSmem = 2 * kFSt + kG2M * kFVRLD;
+constexpr int kFSmem = kFS * kFSt + kG2M * kFVRLD;
 constexpr int kGemmSmem =
     cmax(cmax(kGramPart, kG2S * kG2St - 3 * kSmallMat),
          EIGENID_STAGE1_FUSED ? kFSmem - 2 * kSmallMat : 0);
@@ -60,7 +70,7 @@ static_assert(kG2S * kG2St <= kGemmSmem + 3 * kSmallMat, "gemm2 smem");
 static_assert(!EIGENID_STAGE1_FUSED || kFSmem <= kGemmSmem + 2 * kSmallMat, "fused smem");
 static_assert(kG1S * (kG1_A + kG1_B) <= kGemm1Smem &&
                   kG1S * (kG1_T + kG1_B) <= kGemm1Smem, "gemm1 smem");
-constexpr int kRed = 8 + 8 * kB;
+constexpr int kRed = kNW + kNW * kB;
 // T, G/Y, A persist across Gram calls; B and R live in the GEMM region
 // (never alive across a gram() or GEMM call).  ~101 KB: two CTAs per SM.
 constexpr int kStage1SmemDoubles = kGemmSmem + 3 * kSmallMat + kRed + 4 * kB;
@@ -129,11 +139,11 @@ __device__ void panel_qr(double* P0, int ldw, int s, double* stau, double* red,
     }
     // pass A: acc_q = sum_{r>t} P(r,t) P(r,q)
     double acc = 0.0;
-    for (int r0 = t + 1 + warp; r0 < s; r0 += 32) {
+    for (int r0 = t + 1 + warp; r0 < s; r0 += 4 * kNW) {
       double row[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 8 * u;
+        const int r = r0 + kNW * u;
         row[u] = r < s ? P0[(long long)r * ldw + lane] : 0.0;
       }
 #pragma unroll
@@ -141,12 +151,12 @@ __device__ void panel_qr(double* P0, int ldw, int s, double* stau, double* red,
         acc += __shfl_sync(0xffffffffu, row[u], t) * row[u];
     }
     __syncthreads();
-    red[8 + warp * kB + lane] = acc;
+    red[kNW + warp * kB + lane] = acc;
     __syncthreads();
     if (warp == 0) {
       double w = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < kNT / 32; ++ww) w += red[8 + ww * kB + lane];
+      for (int ww = 0; ww < kNW; ++ww) w += red[kNW + ww * kB + lane];
       w = w * scal + P0[(long long)t * ldw + lane];
       wsm[lane] = (lane > t) ? tau * w : 0.0;
     }
@@ -154,16 +164,16 @@ __device__ void panel_qr(double* P0, int ldw, int s, double* stau, double* red,
     // pass B: P(r,q) -= tau w_q v_r, v stored below the diagonal
     const double wq = wsm[lane];
     loc = 0.0;
-    for (int r0 = t + warp; r0 < s; r0 += 32) {
+    for (int r0 = t + warp; r0 < s; r0 += 4 * kNW) {
       double row[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 8 * u;
+        const int r = r0 + kNW * u;
         row[u] = r < s ? P0[(long long)r * ldw + lane] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 8 * u;
+        const int r = r0 + kNW * u;
         if (r < s) {
           const double x = __shfl_sync(0xffffffffu, row[u], t);
           const double v = (r == t) ? 1.0 : x * scal;
@@ -195,7 +205,7 @@ __device__ void extract_v(const double* P0, int ldw, int s, double* Vg) {
 }
 
 // out[q][p] = sum_{r<s} L(r,q) R(r,p) on the DMMA path: warp w takes the
-// 4-row k-slices i = w (mod 8); partials are summed through shared memory.
+// 4-row k-slices i = w (mod kNW); partials are summed through shared memory.
 __device__ void gram(const double* L, int ldl, const double* R, int ldr, int s,
                      double* out, double* part) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -221,20 +231,35 @@ __device__ void gram(const double* L, int ldl, const double* R, int ldr, int s,
         dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
   }
   __syncthreads();
-  double* pw = part + warp * kSmallMat;
+  // 8 partial slots; with 16 warps, warps 8..15 deposit first and warps
+  // 0..7 add their own partial on top
+  double* pw = part + (warp & 7) * kSmallMat;
+  if (warp >= 8) {
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      pw[(8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk] = acc[mt][nt][0];
-      pw[(8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk + 1] = acc[mt][nt][1];
-    }
+      for (int nt = 0; nt < 4; ++nt) {
+        pw[(8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk] = acc[mt][nt][0];
+        pw[(8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk + 1] = acc[mt][nt][1];
+      }
+  }
+  if (kNW > 8) __syncthreads();
+  if (warp < 8) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double* q0 = pw + (8 * mt + mm) * kSmallLD + 8 * nt + 2 * kk;
+        q0[0] = (kNW > 8 ? q0[0] : 0.0) + acc[mt][nt][0];
+        q0[1] = (kNW > 8 ? q0[1] : 0.0) + acc[mt][nt][1];
+      }
+  }
   __syncthreads();
   for (int e = tid; e < kB * kB; e += kNT) {
     const int q = e / kB, p = e % kB;
     double v = 0.0;
 #pragma unroll
-    for (int w = 0; w < kNT / 32; ++w) v += part[w * kSmallMat + q * kSmallLD + p];
+    for (int w = 0; w < 8; ++w) v += part[w * kSmallMat + q * kSmallLD + p];
     out[q * kSmallLD + p] = v;
   }
   __syncthreads();
@@ -792,7 +817,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
   const int crow = 8 * warp + mm;
-  double* sVr = sm + 2 * kFSt;
+  double* sVr = sm + kFS * kFSt;
   for (int rb = 0; rb < sn; rb += kG2M) {
     const int r = rb + crow;
     double2 af[kG2K / 8];
@@ -813,7 +838,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     auto stage = [&](int ci) {
       if (ci < ncb) {
         const int cb = ci * kG2N;
-        double* st = sm + (ci & 1) * kFSt;
+        double* st = sm + (ci % kFS) * kFSt;
         for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
           const int row = t >> 5, k2 = (t & 31) * 2;
           const int gr = cb + row;
@@ -850,22 +875,23 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       cp_async16(sVr + row * kFVRLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
                  bytes);
     }
-    stage(0);
+#pragma unroll
+    for (int p = 0; p < kFS - 1; ++p) stage(p);
     for (int ci = 0; ci < ncb; ++ci) {
-      cpa_wait0();
+      cpa_wait<kFS - 2>();
       __syncthreads();
-      stage(ci + 1);
+      stage(ci + kFS - 1);
       const int cb = ci * kG2N;
-      const double* b = sm + (ci & 1) * kFSt;
+      const double* b = sm + (ci % kFS) * kFSt;
       double* cs = const_cast<double*>(b) + kG2N * kG2K;
       const double* vc = cs + kG2M * kG2N;
       // X[cb] block of this warp for the transposed product below, loaded
       // early so the read overlaps the rank-2kB update
-      const int mt2 = warp >> 1, nb = 2 * (warp & 1);
+      const int mt2 = warp / (4 / kXT), nb = (warp % (4 / kXT)) * kXT;
       const int xrow = cb + 8 * mt2 + mm;
-      double x2[2][2];
+      double x2[kXT][2];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kXT; ++u) {
         const int xc = 8 * (nb + u) + 2 * kk;
         if (xrow < sn) {
           double2 t;
@@ -933,7 +959,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], a.y, b1[nt]);
       }
-      // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 16 cols)
+      // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 8*kXT cols)
       {
         const int ccol = 8 * mt2 + mm;  // tile column of C = X row
 #pragma unroll 4
@@ -942,12 +968,12 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           const double v = cs[cswz(krow, ccol)];
           const double a = (diag && rb + krow <= cb + ccol) ? 0.0 : v;
 #pragma unroll
-          for (int u = 0; u < 2; ++u)
+          for (int u = 0; u < kXT; ++u)
             dmma(x2[u][0], x2[u][1], a, sVr[krow * kFVRLD + 8 * (nb + u) + mm]);
         }
         if (xrow < sn) {
 #pragma unroll
-          for (int u = 0; u < 2; ++u)
+          for (int u = 0; u < kXT; ++u)
             *reinterpret_cast<double2*>(Xn + (long long)xrow * kB + 8 * (nb + u) + 2 * kk) =
                 make_double2(x2[u][0], x2[u][1]);
         }
@@ -1002,7 +1028,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(kNT, 2) band_reduce_kernel(Stage1Args args) {
+__global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args args) {
 #ifdef EIGENID_PHASE_TIMING
   long long t_ph_ = clock64();
   int ph_ = 0;
@@ -1185,6 +1211,7 @@ extern "C" void eigenid_debug_cta_span(unsigned long long* out) {
 size_t stage1_smem_bytes() { return sizeof(double) * (size_t)kStage1SmemDoubles; }
 int stage1_band_ld() { return kLDAB; }
 int stage1_bandwidth() { return kB; }
+int stage1_ctas_per_sm() { return kCtasPerSm; }
 long long stage1_ws_doubles(int n, int ldw) {
   return (long long)n * ldw + 5LL * n * kB;
 }

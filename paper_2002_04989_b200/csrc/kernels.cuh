@@ -34,6 +34,7 @@ cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
 int stage1_band_ld();
 int stage1_bandwidth();
 long long stage1_ws_doubles(int n, int ldw);  // per-slot workspace
+int stage1_ctas_per_sm();
 
 // ---- bulge.cu: stage 2, band -> tridiagonal
 struct Stage2Args {

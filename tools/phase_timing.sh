@@ -3,7 +3,7 @@
 set -e
 cd $GRAFT_REPO_ROOT
 mkdir -p /tmp/phb
-for f in paper_2002_04989_b200/csrc/*.cu; do nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DEIGENID_PHASE_TIMING -Xcompiler -fPIC -c $f -o /tmp/phb/$(basename $f).o; done
+for f in paper_2002_04989_b200/csrc/*.cu; do nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DEIGENID_PHASE_TIMING $VARIANT -Xcompiler -fPIC -c $f -o /tmp/phb/$(basename $f).o; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o /tmp/phb/libeigenid_b200.so /tmp/phb/*.o
 python - <<'PY'
 import ctypes, sys, os, numpy as np
@@ -20,7 +20,7 @@ buf = (ctypes.c_ulonglong * 16)()
 lib.eigenid_debug_phase_cycles(buf)
 names = ['other', 'copy', 'panel', 'band+VT', 'gemm1', 'Y,M,W2', 'gemm2', '-']
 tot = sum(buf[i] for i in range(8))
-g1 = min(rows + 1, 296)
+g1 = min(rows + 1, int(os.environ.get('SLOTS', '296')))
 print(f'stage 1 (summed over {g1} CTAs, shown per CTA):')
 for i in range(8): print(f'  {names[i]:10s} {buf[i]/g1/1.965e9*1e3:9.2f} ms  {100*buf[i]/max(tot,1):5.1f}%')
 names2 = ['gram P', 'chol+inv', 'row_transform x3', 'gram Q', 'check+chol+mul+inv', '-', 'LU+inv+T+V']
@@ -30,7 +30,7 @@ for i in range(7):
 print(f'  panel_qr fallbacks (all CTAs): {buf[15]}')
 sp = (ctypes.c_ulonglong * 1536)()
 lib.eigenid_debug_cta_span(sp)
-g = min(rows + 1, 296)
+g = min(rows + 1, int(os.environ.get('SLOTS', '296')))
 st = np.array([sp[2 * b] for b in range(g)], dtype=np.float64)
 sm = np.array([sp[1024 + b] for b in range(g)])
 en = np.array([sp[2 * b + 1] for b in range(g)], dtype=np.float64)
