@@ -926,6 +926,27 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
       }
+      const bool diag = cb + kB > rb;  // the tile may cross the diagonal
+      // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators: the
+      // m8n8k4 accumulator of column tile q holds C[row][8q+2kk .. +1], which
+      // is exactly this lane's A-fragment pair for k-pair q (no shared-memory
+      // round trip, no barrier)
+#pragma unroll
+      for (int q = 0; q < kB / 8; ++q) {
+        const int k = 8 * q + 2 * kk;
+        const double ax = (diag && cb + k > r) ? 0.0 : acc[q][0];
+        const double ay = (diag && cb + k + 1 > r) ? 0.0 : acc[q][1];
+        double b0[kG2N / 8], b1[kG2N / 8];
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          b0[nt] = vc[k * kFVLD + 8 * nt + mm];
+          b1[nt] = vc[(k + 1) * kFVLD + 8 * nt + mm];
+        }
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], ax, b0[nt]);
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], ay, b1[nt]);
+      }
 #pragma unroll
       for (int nt = 0; nt < kG2N / 8; ++nt) {
         const int col = cb + 8 * nt + 2 * kk;
@@ -940,25 +961,6 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
             make_double2(acc[nt][0], acc[nt][1]);
       }
       __syncthreads();
-      const bool diag = cb + kB > rb;  // the tile may cross the diagonal
-      // ---- X[rb] += tril(C) VTn[cb]   (this lane's row, k = tile columns)
-#pragma unroll
-      for (int q = 0; q < kB / 8; ++q) {
-        const int k = 8 * q + 2 * kk;
-        double2 a = *reinterpret_cast<const double2*>(cs + cswz(crow, k));
-        if (diag && cb + k > r) a.x = 0.0;
-        if (diag && cb + k + 1 > r) a.y = 0.0;
-        double b0[kG2N / 8], b1[kG2N / 8];
-#pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) {
-          b0[nt] = vc[k * kFVLD + 8 * nt + mm];
-          b1[nt] = vc[(k + 1) * kFVLD + 8 * nt + mm];
-        }
-#pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], a.x, b0[nt]);
-#pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], a.y, b1[nt]);
-      }
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 8*kXT cols)
       {
         const int ccol = 8 * mt2 + mm;  // tile column of C = X row
