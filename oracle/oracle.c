@@ -590,3 +590,118 @@ int orc_all_magnitudes(const double* a, size_t n, size_t batch, double tol,
   free(mu);
   return st;
 }
+
+/* ---- sign recovery ------------------------------------------------------
+ * Restates recover_signs (src/signs.cpp:48-120) and its Gaussian elimination
+ * with partial pivoting (solve_linear, :13-44): the largest magnitude (first
+ * on ties) anchors the vector, the other n-1 row equations of
+ * (A - lambda I) v = 0 are solved for the remaining components, only their
+ * signs are kept, the first component above sign_tol is made positive and the
+ * residual ||(A - lambda I) v|| is checked against 1e-6 ||A||_F. */
+static int orc_gauss_solve(double* w, double* rhs, size_t m) {
+  for (size_t col = 0; col < m; ++col) {
+    size_t piv = col;
+    for (size_t r = col + 1; r < m; ++r)
+      if (fabs(w[r * m + col]) > fabs(w[piv * m + col])) piv = r;
+    if (w[piv * m + col] == 0.0) return 0;
+    if (piv != col) {
+      for (size_t c = 0; c < m; ++c) {
+        const double t = w[col * m + c];
+        w[col * m + c] = w[piv * m + c];
+        w[piv * m + c] = t;
+      }
+      const double t = rhs[col];
+      rhs[col] = rhs[piv];
+      rhs[piv] = t;
+    }
+    const double inv = 1.0 / w[col * m + col];
+    for (size_t r = col + 1; r < m; ++r) {
+      const double f = w[r * m + col] * inv;
+      if (f == 0.0) continue;
+      for (size_t c = col; c < m; ++c) w[r * m + c] -= f * w[col * m + c];
+      rhs[r] -= f * rhs[col];
+    }
+  }
+  for (size_t col = m; col-- > 0;) {
+    double acc = rhs[col];
+    for (size_t c = col + 1; c < m; ++c) acc -= w[col * m + c] * rhs[c];
+    rhs[col] = acc / w[col * m + col];
+  }
+  return 1;
+}
+
+int orc_recover_signs(const double* a, size_t n, size_t i, const double* mags,
+                      size_t nmags, double lambda_i, double sign_tol,
+                      double* out, orc_err* err) {
+  (void)i; /* unused by the reference too (signs.cpp:54) */
+  if (nmags != n) {
+    set_err(err, ORC_E_DIMENSION, -1, 0.0, "magnitude vector length does not match n");
+    return ORC_E_DIMENSION;
+  }
+  for (size_t j = 0; j < n; ++j) {
+    const double c = mags[j] < 0.0 ? 0.0 : (mags[j] > 1.0 ? 1.0 : mags[j]);
+    out[j] = sqrt(c);
+  }
+  if (n > 1) {
+    size_t anchor = 0;
+    for (size_t j = 1; j < n; ++j)
+      if (mags[j] > mags[anchor]) anchor = j;
+    const size_t m = n - 1;
+    double* w = (double*)malloc(sizeof(double) * m * m);
+    double* rhs = (double*)malloc(sizeof(double) * m);
+    if (!w || !rhs) {
+      free(w);
+      free(rhs);
+      set_err(err, ORC_E_ALLOC, -1, 0.0, "allocation failed");
+      return ORC_E_ALLOC;
+    }
+    size_t rr = 0;
+    for (size_t r = 0; r < n; ++r) {
+      if (r == anchor) continue;
+      size_t cc = 0;
+      for (size_t c = 0; c < n; ++c) {
+        if (c == anchor) continue;
+        w[rr * m + cc] = a[r * n + c] - (r == c ? lambda_i : 0.0);
+        ++cc;
+      }
+      rhs[rr] = -(a[r * n + anchor] - (r == anchor ? lambda_i : 0.0)) * out[anchor];
+      ++rr;
+    }
+    const int ok = orc_gauss_solve(w, rhs, m);
+    if (!ok) {
+      free(w);
+      free(rhs);
+      set_err(err, ORC_E_SIGN_RECOVERY, -1, 0.0, "row equations are singular at the anchor");
+      return ORC_E_SIGN_RECOVERY;
+    }
+    rr = 0;
+    for (size_t r = 0; r < n; ++r) {
+      if (r == anchor) continue;
+      if (mags[r] > sign_tol && rhs[rr] < 0.0) out[r] = -out[r];
+      ++rr;
+    }
+    free(w);
+    free(rhs);
+  }
+  for (size_t j = 0; j < n; ++j)
+    if (mags[j] > sign_tol) {
+      if (out[j] < 0.0)
+        for (size_t t = 0; t < n; ++t) out[t] = -out[t];
+      break;
+    }
+  double res2 = 0.0, fro2 = 0.0;
+  for (size_t r = 0; r < n; ++r) {
+    double row = 0.0;
+    for (size_t c = 0; c < n; ++c) row += (a[r * n + c] - (r == c ? lambda_i : 0.0)) * out[c];
+    res2 += row * row;
+  }
+  for (size_t t = 0; t < n * n; ++t) fro2 += a[t] * a[t];
+  const double res = sqrt(res2), bound = 1e-6 * sqrt(fro2);
+  if (res > bound) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "sign recovery residual %f exceeds %f", res, bound);
+    set_err(err, ORC_E_SIGN_RECOVERY, -1, 0.0, buf);
+    return ORC_E_SIGN_RECOVERY;
+  }
+  return ORC_OK;
+}

@@ -32,6 +32,8 @@ enum {
   ORC_E_INTERNAL = 5,          /* InternalInconsistency errors.hpp:74-77 */
   ORC_E_CONFIG = 6,            /* ConfigError          errors.hpp:89-92 */
   ORC_E_INDEX = 7,             /* IndexOutOfRange      errors.hpp:26-29 */
+  ORC_E_SIGN_RECOVERY = 8,     /* SignRecoveryFailure  errors.hpp:79-82 */
+  ORC_E_DIMENSION = 9,         /* DimensionMismatch    errors.hpp:46-49 */
   ORC_E_ALLOC = 30
 };
 
@@ -88,6 +90,12 @@ int orc_all_magnitudes(const double* a, size_t n, size_t batch, double tol,
                        double* lambda_out, double* mu_out, orc_err* err);
 /* Minor spectra for a list of minor indices, one minor per thread
  * (identity.cpp:303-306). mu is count x (n-1). */
+/* ---- sign recovery: src/signs.cpp:48-120 ---- */
+/* Signed eigenvector from squared magnitudes (n entries in out). */
+int orc_recover_signs(const double* a, size_t n, size_t i, const double* mags,
+                      size_t nmags, double lambda_i, double sign_tol,
+                      double* out, orc_err* err);
+
 int orc_minor_spectra(const double* a, size_t n, const size_t* js,
                       size_t count, int threads, double* mu, orc_err* err);
 

@@ -72,6 +72,8 @@ class Oracle:
         L.orc_all_magnitudes.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_double,
                                          C.c_int, C.c_int, _dp, _dp, _dp,
                                          C.POINTER(OrcErr)]
+        L.orc_recover_signs.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t,
+                                         C.c_double, C.c_double, _dp, C.POINTER(OrcErr)]
         L.orc_minor_spectra.argtypes = [_dp, C.c_size_t, _szp, C.c_size_t,
                                         C.c_int, _dp, C.POINTER(OrcErr)]
 
@@ -192,6 +194,17 @@ class Oracle:
             return out, lam[:n], mu[: n * (n - 1)].reshape(n, n - 1)
         return out
 
+    def recover_signs(self, a, i, mags, lambda_i, sign_tol=1e-10):
+        """signs.cpp:48-120."""
+        a = np.ascontiguousarray(a, np.float64)
+        n = a.shape[0]
+        mags = np.ascontiguousarray(mags, np.float64)
+        out = np.empty(n)
+        err = OrcErr()
+        _check(self.lib.orc_recover_signs(_p(a), n, i, _p(mags), mags.size, lambda_i,
+                                        sign_tol, _p(out), C.byref(err)), err)
+        return out
+
     def minor_spectra(self, a, js, threads=None):
         a = np.ascontiguousarray(a, np.float64)
         n = a.shape[0]
@@ -226,6 +239,8 @@ class Reference:
         L.ref_identity_rows.argtypes = [_dp, _dp, C.c_size_t, C.c_size_t,
                                         C.c_size_t, C.c_double, C.c_size_t, _dp, E]
         L.ref_jacobi.argtypes = [_dp, C.c_size_t, _dp, _dp, E]
+        L.ref_recover_signs.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t,
+                                        C.c_double, C.c_double, _dp, E]
 
     def random_symmetric(self, seed, n, uniform=False):
         out = np.empty((n, n), np.float64)
@@ -290,6 +305,16 @@ class Reference:
         _check(self.lib.ref_identity_rows(_p(lam), _p(mu_rows), n, mu_rows.shape[0],
                                           batch, tol, workers or os.cpu_count() or 1,
                                           _p(out), C.byref(err)), err)
+        return out
+
+    def recover_signs(self, a, i, mags, lambda_i, sign_tol=1e-10):
+        a = np.ascontiguousarray(a, np.float64)
+        n = a.shape[0]
+        mags = np.ascontiguousarray(mags, np.float64)
+        out = np.empty(n)
+        err = OrcErr()
+        _check(self.lib.ref_recover_signs(_p(a), n, i, _p(mags), mags.size, lambda_i,
+                                        sign_tol, _p(out), C.byref(err)), err)
         return out
 
     def jacobi(self, a, vectors=True):

@@ -64,6 +64,12 @@ int guarded(RefErr* err, F&& f) {
   } catch (const IndexOutOfRange& e) {
     fill(err, 7, 0.0, e.what());
     return 7;
+  } catch (const SignRecoveryFailure& e) {
+    fill(err, 8, 0.0, e.what());
+    return 8;
+  } catch (const DimensionMismatch& e) {
+    fill(err, 9, 0.0, e.what());
+    return 9;
   } catch (const std::exception& e) {
     fill(err, 29, 0.0, e.what());
     return 29;
@@ -197,6 +203,17 @@ int ref_jacobi(const double* a, std::size_t n, double* evals, double* evecs,
     auto dec = jacobi_eigendecomposition(wrap(a, n));
     std::memcpy(evals, dec.spectrum.values.data(), n * sizeof(double));
     if (evecs) std::memcpy(evecs, dec.vectors.data(), n * n * sizeof(double));
+  });
+}
+
+// recover_signs (signs.cpp:48-120): signed eigenvector i from magnitudes.
+int ref_recover_signs(const double* a, std::size_t n, std::size_t i,
+                      const double* mags, std::size_t nmags, double lambda_i,
+                      double sign_tol, double* out, RefErr* err) {
+  return guarded(err, [&] {
+    const auto v = recover_signs(wrap(a, n), i, std::vector<double>(mags, mags + nmags),
+                                 lambda_i, sign_tol);
+    std::memcpy(out, v.data(), n * sizeof(double));
   });
 }
 

@@ -69,6 +69,20 @@ def main():
     out["c5_rows"] = np.array(rows)
     out["c5_mu_8192"] = mu
     out["c5_id_8192"] = ref.identity_rows(lam, mu, workers=0)
+    # sign recovery (signs.cpp:48-120): every eigenvector of small seeded
+    # matrices, magnitudes and eigenvalues from the reference itself
+    for n, seed in ((15, 8), (33, 21), (100, 77)):
+        a = ref.random_symmetric(seed, n)
+        lam = ref.eigenvalues(a)
+        mags = ref.all_magnitudes(a, workers=1).reshape(n, n)
+        out[f"signs_n{n}_a"] = a
+        out[f"signs_n{n}_lam"] = lam
+        out[f"signs_n{n}_mags"] = mags
+        out[f"signs_n{n}_v"] = np.stack([ref.recover_signs(a, i, mags[:, i], lam[i])
+                                         for i in range(n)])
+    out["signs_hand_2x2"] = ref.recover_signs(np.array([[2.0, 1.0], [1.0, 2.0]]), 0,
+                                              [0.5, 0.5], 1.0)
+    out["signs_hand_diag"] = ref.recover_signs(np.diag([1.0, 2.0]), 1, [0.0, 1.0], 2.0)
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", len(out), "arrays")
 

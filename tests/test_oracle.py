@@ -137,3 +137,42 @@ def test_doubly_stochastic(oracle):
     m = oracle.all_magnitudes(oracle.random_symmetric(77, 100))
     assert np.max(np.abs(m.sum(0) - 1)) <= 1e-8
     assert np.max(np.abs(m.sum(1) - 1)) <= 1e-8
+
+
+# ---------------------------------------------------------------- signs (f4)
+def test_recover_signs_golden(oracle, gold):
+    """signs.cpp:48-120 restated: every eigenvector of three seeded matrices
+    bit-identical to the reference's recover_signs (golden vectors)."""
+    for n in (15, 33, 100):
+        a, lam, mags = gold[f"signs_n{n}_a"], gold[f"signs_n{n}_lam"], gold[f"signs_n{n}_mags"]
+        want = gold[f"signs_n{n}_v"]
+        for i in range(n):
+            got = oracle.recover_signs(a, i, mags[:, i], lam[i])
+            assert np.array_equal(got.view(np.uint64), want[i].view(np.uint64)), (n, i)
+
+
+def test_recover_signs_hand_cases_and_errors(oracle, gold):
+    """test_identity.cpp:313-354 known answers and error behaviour."""
+    v = oracle.recover_signs(np.array([[2.0, 1.0], [1.0, 2.0]]), 0, [0.5, 0.5], 1.0)
+    assert np.array_equal(v, gold["signs_hand_2x2"])
+    assert abs(v[0] - 2 ** -0.5) < 1e-12 and abs(v[1] + 2 ** -0.5) < 1e-12
+    v = oracle.recover_signs(np.diag([1.0, 2.0]), 1, [0.0, 1.0], 2.0)
+    assert np.array_equal(v, gold["signs_hand_diag"])
+    a = oracle.random_symmetric(8, 10)
+    with pytest.raises(OracleError) as e:
+        oracle.recover_signs(a, 0, np.full(10, 0.1), 123.0)
+    assert e.value.code == 8  # SignRecoveryFailure
+    with pytest.raises(OracleError) as e:
+        oracle.recover_signs(a, 0, np.full(9, 0.1), 123.0)
+    assert e.value.code == 9  # DimensionMismatch
+
+
+def test_recover_signs_matches_reference_live(oracle, reference):
+    for n, seed in ((5, 3), (40, 4), (64, 5)):
+        a = reference.random_symmetric(seed, n)
+        lam = reference.eigenvalues(a)
+        mags = reference.all_magnitudes(a, workers=1).reshape(n, n)
+        for i in range(0, n, 3):
+            want = reference.recover_signs(a, i, mags[:, i], lam[i])
+            got = oracle.recover_signs(a, i, mags[:, i], lam[i])
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
