@@ -29,6 +29,7 @@ EIGENID_ERROR(ConvergenceFailure)
 EIGENID_ERROR(NonFiniteIntermediate)
 EIGENID_ERROR(InternalInconsistency)
 EIGENID_ERROR(ConfigError)
+EIGENID_ERROR(SignRecoveryFailure)
 #undef EIGENID_ERROR
 
 // Repeated eigenvalue of A: components are not unique (errors.hpp:58-66).

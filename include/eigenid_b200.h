@@ -43,6 +43,8 @@ enum eigenid_status {
   EIGENID_E_INTERNAL = 5,         /* InternalInconsistency errors.hpp:74-77 */
   EIGENID_E_CONFIG = 6,           /* ConfigError           errors.hpp:89-92 */
   EIGENID_E_INDEX = 7,            /* IndexOutOfRange       errors.hpp:26-29 */
+  EIGENID_E_SIGN_RECOVERY = 8,    /* SignRecoveryFailure   errors.hpp:79-82 */
+  EIGENID_E_DIMENSION = 9,        /* DimensionMismatch     errors.hpp:46-49 */
   EIGENID_E_DEVICE = 20,          /* new: CUDA failure / no device          */
   EIGENID_E_ALLOC = 21            /* new: device allocation failed          */
 };
@@ -133,12 +135,32 @@ int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* ctx, const double* a,
                                     double* value, double* raw, int* method,
                                     eigenid_gpu_err* err);
 
+/* Sign recovery (recover_signs, signs.cpp:48-120; identity.hpp:159-166):
+ * the signed eigenvector i from its squared magnitudes (n_magnitudes must
+ * equal n, else EIGENID_E_DIMENSION) and lambda_i.  The largest magnitude is
+ * anchored, the other n-1 row equations of (A - lambda_i I) v = 0 are solved
+ * on the device (blocked LU with partial pivoting), only their signs are
+ * kept, the first component above sign_tol is made positive.  A zero pivot
+ * or a residual above 1e-6 ||A||_F is EIGENID_E_SIGN_RECOVERY.  `i` is
+ * accepted for interface parity and unused, as in the reference. */
+int eigenid_gpu_recover_signs(eigenid_gpu_ctx* ctx, const double* a, size_t n,
+                              size_t i, const double* magnitudes,
+                              size_t n_magnitudes, double lambda_i,
+                              double sign_tol, double* out_v,
+                              eigenid_gpu_err* err);
+
 /* Reference-style per-call instrumentation: eigenvalue solves performed by
  * this context (identity.hpp:137-144).  all_magnitudes adds n+1. */
 size_t eigenid_gpu_solve_count(eigenid_gpu_ctx* ctx);
 void eigenid_gpu_reset_solve_count(eigenid_gpu_ctx* ctx);
 
 /* ---- device-pointer entry points (inputs resident in HBM) ------------ */
+
+/* recover_signs on device-resident A (n x n), magnitudes (n) and d_out (n). */
+int eigenid_gpu_recover_signs_device(eigenid_gpu_ctx* ctx, const double* d_a,
+                                     size_t n, const double* d_magnitudes,
+                                     double lambda_i, double sign_tol,
+                                     double* d_out, eigenid_gpu_err* err);
 
 /* Full pipeline for minor rows j0..j1-1 of a device-resident A: computes
  * lambda(A) (redundantly per shard) and the minor spectra, then the identity

@@ -9,15 +9,15 @@ C++ API over that boundary.
 from .errors import (AsymmetricInput, ConfigError, ConvergenceFailure,  # noqa: F401
                      DegenerateEigenvalue, DeviceError, DimensionMismatch, Error,
                      IndexOutOfRange, InternalInconsistency, MatrixTooSmall,
-                     NonFiniteEntry, NonFiniteIntermediate)
+                     NonFiniteEntry, NonFiniteIntermediate, SignRecoveryFailure)
 from .engine import (Device, IdentityConfig, IdentityEngine,  # noqa: F401
-                     SymmetricMatrix, eigenvalues, random_symmetric)
+                     SymmetricMatrix, eigenvalues, random_symmetric, recover_signs)
 
 __all__ = [
     "IdentityEngine", "IdentityConfig", "SymmetricMatrix", "eigenvalues", "Device",
-    "random_symmetric",
+    "random_symmetric", "recover_signs",
     "Error", "MatrixTooSmall", "DegenerateEigenvalue", "ConvergenceFailure",
     "NonFiniteIntermediate", "InternalInconsistency", "ConfigError",
     "IndexOutOfRange", "DeviceError", "AsymmetricInput", "NonFiniteEntry",
-    "DimensionMismatch",
+    "DimensionMismatch", "SignRecoveryFailure",
 ]

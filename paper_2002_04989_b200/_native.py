@@ -51,6 +51,12 @@ SIGNATURES = {
     "eigenid_gpu_vector_magnitudes": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t,
                                                 C.POINTER(GpuConfig), _dp, _dp,
                                                 C.POINTER(GpuErr)]),
+    "eigenid_gpu_recover_signs": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t, _dp,
+                                            C.c_size_t, C.c_double, C.c_double, _dp,
+                                            C.POINTER(GpuErr)]),
+    "eigenid_gpu_recover_signs_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t,
+                                                   C.c_void_p, C.c_double, C.c_double,
+                                                   C.c_void_p, C.POINTER(GpuErr)]),
     "eigenid_gpu_component_magnitude": (C.c_int, [C.c_void_p, _dp, C.c_size_t,
                                                   C.c_size_t, C.c_size_t, _dp, _dp,
                                                   C.POINTER(GpuConfig), _dp, _dp,

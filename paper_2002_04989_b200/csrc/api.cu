@@ -847,6 +847,84 @@ int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
   return EIGENID_OK;
 }
 
+// ---- sign recovery (signs.cpp:48-120) ------------------------------------
+namespace {
+int recover_impl(eigenid_gpu_ctx* c, const double* dA, size_t n, const double* dm,
+                 double lambda_i, double sign_tol, double* dv, eigenid_gpu_err* err) {
+  EID_CUDA(c->bWs.ensure(sizeof(double) * (size_t)recover_ws_doubles((int)n)), "alloc ws");
+  EID_CUDA(c->bCounter.ensure(recover_state_bytes() > 16 ? recover_state_bytes() : 16),
+           "alloc state");
+  auto* stp = reinterpret_cast<RecoverState*>(c->bCounter.p);
+  int launches = 0;
+  EID_CUDA(launch_recover_signs(dA, (int)n, dm, lambda_i, sign_tol, dv, c->bWs.as<double>(),
+                                stp, c->stream, &launches),
+           "recover_signs");
+  c->launches += launches;
+  RecoverResult r;
+  EID_CUDA(recover_result(stp, &r, c->stream), "recover state");
+  if (r.singular) {
+    set_err(err, EIGENID_E_SIGN_RECOVERY, -1, 0.0, 0,
+            "row equations are singular at the anchor");
+    return EIGENID_E_SIGN_RECOVERY;
+  }
+  const double res = std::sqrt(r.res2), bound = 1e-6 * std::sqrt(r.fro2);
+  if (res > bound) {  // signs.cpp:113-118 (std::to_string formatting)
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "sign recovery residual %f exceeds %f", res, bound);
+    set_err(err, EIGENID_E_SIGN_RECOVERY, -1, 0.0, 0, buf);
+    return EIGENID_E_SIGN_RECOVERY;
+  }
+  return EIGENID_OK;
+}
+}  // namespace
+
+int eigenid_gpu_recover_signs(eigenid_gpu_ctx* c, const double* a, size_t n, size_t i,
+                              const double* magnitudes, size_t n_magnitudes,
+                              double lambda_i, double sign_tol, double* out_v,
+                              eigenid_gpu_err* err) {
+  (void)i;  // unused by the reference too (signs.cpp:54)
+  if (n_magnitudes != n) {
+    set_err(err, EIGENID_E_DIMENSION, -1, 0.0, 0, "magnitude vector length does not match n");
+    return EIGENID_E_DIMENSION;
+  }
+  if (n == 0) return EIGENID_OK;
+  if (n > 14000) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "n exceeds the device limit (14000)");
+    return EIGENID_E_CONFIG;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  int st;
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc mags");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * n), "alloc out");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n, cudaMemcpyHostToDevice,
+                           c->stream), "H2D A");
+  EID_CUDA(cudaMemcpyAsync(c->bLam.p, magnitudes, sizeof(double) * n, cudaMemcpyHostToDevice,
+                           c->stream), "H2D mags");
+  st = recover_impl(c, c->bA.as<double>(), n, c->bLam.as<double>(), lambda_i, sign_tol,
+                    c->bOut.as<double>(), err);
+  if (st) return st;
+  EID_CUDA(cudaMemcpyAsync(out_v, c->bOut.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                           c->stream), "D2H v");
+  EID_CUDA(cudaStreamSynchronize(c->stream), "sync");
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_recover_signs_device(eigenid_gpu_ctx* c, const double* d_a, size_t n,
+                                     const double* d_magnitudes, double lambda_i,
+                                     double sign_tol, double* d_out, eigenid_gpu_err* err) {
+  if (n == 0) return EIGENID_OK;
+  if (n > 14000) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "n exceeds the device limit (14000)");
+    return EIGENID_E_CONFIG;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  int st;
+  if ((st = begin(c, err))) return st;
+  return recover_impl(c, d_a, n, d_magnitudes, lambda_i, sign_tol, d_out, err);
+}
+
 int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* c, const double* a,
                                     size_t n, size_t i, size_t j,
                                     const double* lambda, const double* mu_j,

@@ -90,4 +90,19 @@ cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
                           int batch, double* draw, DevStatus* dstatus,
                           cudaStream_t st, int* launches);
 
+// ---- recover.cu: sign recovery (signs.cpp:48-120)
+struct RecoverState;
+long long recover_ws_doubles(int n);
+size_t recover_state_bytes();
+cudaError_t launch_recover_signs(const double* dA, int n, const double* dmags,
+                                 double lambda, double sign_tol, double* dv,
+                                 double* dws, RecoverState* st_dev, cudaStream_t s,
+                                 int* launches);
+// host view of the state the epilogue needs
+struct RecoverResult {
+  int singular;
+  double res2, fro2;
+};
+cudaError_t recover_result(const RecoverState* st_dev, RecoverResult* out, cudaStream_t s);
+
 }  // namespace eigenid_b200

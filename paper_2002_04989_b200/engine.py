@@ -223,6 +223,24 @@ def eigenvalues(a, device: int = 0) -> np.ndarray:
     return out
 
 
+def recover_signs(a, i: int, magnitudes, lambda_i: float, sign_tol: float = 1e-10,
+                  device: int = 0) -> np.ndarray:
+    """recover_signs (identity.hpp:159-166, signs.cpp:48-120): the signed
+    eigenvector i from its squared magnitudes, solved on the GPU.  Raises
+    DimensionMismatch for a wrong-length magnitude vector and
+    SignRecoveryFailure for a singular anchor system or a residual above
+    1e-6 ||A||_F, as the reference does."""
+    n, e = _as_matrix(a)
+    mags = np.ascontiguousarray(magnitudes, np.float64).reshape(-1)
+    dev = Device.get(device)
+    out = np.empty(n, np.float64)
+    err = _native.GpuErr()
+    _native.check(dev.lib.eigenid_gpu_recover_signs(
+        dev.ctx, _native.dptr(e), n, i, _native.dptr(mags), mags.size, lambda_i,
+        sign_tol, _native.dptr(out), C.byref(err)), err)
+    return out
+
+
 class IdentityEngine:
     """identity.hpp:99-157, the all-magnitudes path on the GPU."""
 

@@ -57,6 +57,10 @@ class ConfigError(Error):
     pass
 
 
+class SignRecoveryFailure(Error):
+    """errors.hpp:79-82 (recover_signs)."""
+
+
 class DeviceError(Error):
     """New: a CUDA failure or a missing device (no CPU fallback)."""
 
@@ -73,6 +77,8 @@ _CODES = {
     5: InternalInconsistency,
     6: ConfigError,
     7: IndexOutOfRange,
+    8: SignRecoveryFailure,
+    9: DimensionMismatch,
 }
 
 

@@ -25,6 +25,8 @@ namespace {
     case EIGENID_E_INTERNAL: throw InternalInconsistency(msg);
     case EIGENID_E_CONFIG: throw ConfigError(msg);
     case EIGENID_E_INDEX: throw IndexOutOfRange(msg);
+    case EIGENID_E_SIGN_RECOVERY: throw SignRecoveryFailure(msg);
+    case EIGENID_E_DIMENSION: throw DimensionMismatch(msg);
     default: throw DeviceError(msg, e.cuda_error);
   }
 }
@@ -163,6 +165,19 @@ std::vector<double> IdentityEngine::all_magnitudes_batched(
   solves_ += eigenid_gpu_solve_count(ctx_) - before;
   check(st, e);
   return out;
+}
+
+// ---- recover_signs
+std::vector<double> recover_signs(const SymmetricMatrix& a, std::size_t i,
+                                  const std::vector<double>& magnitudes,
+                                  double lambda_i, double sign_tol) {
+  std::vector<double> v(a.n());
+  eigenid_gpu_err e{};
+  check(eigenid_gpu_recover_signs(shared_ctx(0), a.entries().data(), a.n(), i,
+                                  magnitudes.data(), magnitudes.size(), lambda_i,
+                                  sign_tol, v.data(), &e),
+        e);
+  return v;
 }
 
 }  // namespace eigenid

@@ -72,5 +72,22 @@ int main() {
     for (double v : s.values) sum += v;
     report("eigenvalues-trace", std::fabs(tr - sum) <= 1e-11 && s.n() == n);
   }
+  {  // recover_signs hand cases (test_identity.cpp:313-323) and errors (:350-354)
+    auto v = recover_signs(SymmetricMatrix::build(2, {2, 1, 1, 2}), 0, {0.5, 0.5}, 1.0);
+    const double s = 1.0 / std::sqrt(2.0);
+    bool ok = std::fabs(v[0] - s) <= 1e-12 && std::fabs(v[1] + s) <= 1e-12;
+    auto vd = recover_signs(SymmetricMatrix::diagonal({1, 2}), 1, {0.0, 1.0}, 2.0);
+    ok = ok && vd[0] == 0.0 && vd[1] == 1.0;
+    report("recover-signs", ok);
+    bool a = false, b = false;
+    std::vector<double> junk(10, 0.1);
+    std::vector<double> e(100);
+    for (int r = 0; r < 10; ++r)
+      for (int c = 0; c < 10; ++c) e[r * 10 + c] = (r == c) ? r : 0.1 * (r + c);
+    auto m = SymmetricMatrix::build(10, e);
+    try { recover_signs(m, 0, junk, 123.0); } catch (const SignRecoveryFailure&) { a = true; }
+    try { recover_signs(m, 0, std::vector<double>(9, 0.1), 123.0); } catch (const DimensionMismatch&) { b = true; }
+    report("recover-signs-errors", a && b);
+  }
   return failures;
 }

@@ -319,3 +319,52 @@ def test_component_magnitude_errors(oracle):
         eng.component_magnitude(np.eye(5), 0, 0)
     with pytest.raises(eid.DegenerateEigenvalue):
         eng.vector_magnitudes(np.eye(5), 0)
+
+
+# ------------------------------------------------------------- f4 signs
+def test_recover_signs_golden_bit_exact(gold):
+    """recover_signs on the device vs the reference's golden signed vectors:
+    magnitudes are sqrt(clamp(m)) on both sides and the signs come from the
+    anchored solve, so every eigenvector is bit-identical."""
+    from paper_2002_04989_b200 import recover_signs
+    for n in (15, 33, 100):
+        a, lam, mags = gold[f"signs_n{n}_a"], gold[f"signs_n{n}_lam"], gold[f"signs_n{n}_mags"]
+        want = gold[f"signs_n{n}_v"]
+        for i in range(n):
+            got = recover_signs(a, i, mags[:, i], lam[i])
+            assert np.array_equal(bits(got), bits(want[i])), (n, i)
+
+
+def test_recover_signs_hand_cases_and_errors(gold):
+    """test_identity.cpp:313-354: hand cases, SignRecoveryFailure on
+    inconsistent magnitudes, DimensionMismatch on a wrong length."""
+    from paper_2002_04989_b200 import (DimensionMismatch, SignRecoveryFailure,
+                                       random_symmetric, recover_signs)
+    assert np.array_equal(recover_signs(np.array([[2.0, 1.0], [1.0, 2.0]]), 0, [0.5, 0.5], 1.0),
+                          gold["signs_hand_2x2"])
+    assert np.array_equal(recover_signs(np.diag([1.0, 2.0]), 1, [0.0, 1.0], 2.0),
+                          gold["signs_hand_diag"])
+    a = random_symmetric(8, 10)
+    with pytest.raises(SignRecoveryFailure):
+        recover_signs(a, 0, np.full(10, 0.1), 123.0)
+    with pytest.raises(DimensionMismatch):
+        recover_signs(a, 0, np.full(9, 0.1), 123.0)
+    # n = 1: the magnitude itself, residual |a - lambda| checked
+    assert np.array_equal(recover_signs(np.array([[3.0]]), 0, [1.0], 3.0), [1.0])
+
+
+@pytest.mark.parametrize("n", [257, 700])
+def test_recover_signs_large_vs_oracle(engine, oracle, n):
+    """Blocked device LU (many panels) vs the oracle's unblocked elimination:
+    identical signed vectors on the GPU's own magnitudes and spectrum."""
+    from paper_2002_04989_b200 import eigenvalues, recover_signs
+    a = oracle.random_symmetric(900 + n, n)
+    lam = eigenvalues(a)
+    mags = engine.all_magnitudes(a).reshape(n, n)
+    for i in (0, n // 3, n - 1):
+        got = recover_signs(a, i, mags[:, i], lam[i])
+        want = oracle.recover_signs(a, i, mags[:, i], lam[i])
+        assert np.array_equal(bits(got), bits(want)), i
+        # an eigenvector: unit norm and (A - lambda I) v small
+        assert abs(np.dot(got, got) - 1.0) < 1e-9
+        assert np.linalg.norm(a @ got - lam[i] * got) <= 1e-6 * np.linalg.norm(a)
