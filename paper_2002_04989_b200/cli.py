@@ -6,7 +6,7 @@ is a new driver over the same semantics):
 
     python -m paper_2002_04989_b200.cli full      --random N [--seed S] [--dist gaussian|uniform]
                                                   [--csv F | --mm F] [--out F.csv]
-    python -m paper_2002_04989_b200.cli vector    -i I  <source> [--out F.csv]
+    python -m paper_2002_04989_b200.cli vector    -i I  <source> [--out F.csv] [--signs]
     python -m paper_2002_04989_b200.cli component -i I -j J <source>
     python -m paper_2002_04989_b200.cli bench     --sizes 100 250 ... [--reps R]
                                                   [--task all-vectors] [--seed S]
@@ -15,7 +15,8 @@ is a new driver over the same semantics):
 Engine flags: --batch-size, --workers (accepted, no device meaning),
 --log-domain, --degeneracy-tol.  Output: %.12g on stdout, %.17g in CSV files,
 row j / column i for `full` (eigenid.cpp:151-176), "j,magnitude" for
-`vector` (:139-147); bench records "n,variant,task,run,seconds,checksum"
+`vector` (:139-147), `--signs` prints the signed vector (:129-134,
+recover_signs); bench records "n,variant,task,run,seconds,checksum"
 (bench.cpp:359-372) and plot data "n,variant,mean_seconds,stddev_seconds"
 (bench.cpp:334-357) with variant "gpu-b200".  Exit codes as the reference
 (eigenid.cpp:340-350): 0 ok, 1 library error (DegenerateEigenvalue prints the
@@ -147,6 +148,12 @@ def run_vector(args) -> int:
     if args.i >= n:
         return usage_error(f"index i={args.i} out of range for n = {n}")
     v = _engine(args).vector_magnitudes(a, args.i)
+    if args.signs:  # eigenid.cpp:129-134: signed vector, %.12g per line
+        from .engine import eigenvalues, recover_signs
+        s = eigenvalues(a)
+        for x in recover_signs(a, args.i, v, s[args.i]):
+            print(fmt12(x))
+        return 0
     if args.out:
         with open(args.out, "w") as f:
             f.write("j,magnitude\n")
@@ -264,6 +271,8 @@ def build_parser() -> argparse.ArgumentParser:
     source(p), engine(p)
     p.add_argument("-i", type=int, required=True)
     p.add_argument("--out")
+    p.add_argument("--signs", action="store_true",
+                   help="recover component signs from the row equations")
     p = sub.add_parser("full")
     source(p), engine(p)
     p.add_argument("--out")

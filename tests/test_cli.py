@@ -58,6 +58,13 @@ def test_cli_full_vector_component_bench(tmp_path, oracle, capsys):
                      "--out", str(vec)]) == 0
     assert open(vec).readline().strip() == "j,magnitude"
     capsys.readouterr()
+    # --signs (eigenid.cpp:129-134): the signed eigenvector, %.12g per line
+    assert cli.main(["vector", "-i", "4", "--random", "12", "--seed", "3", "--signs"]) == 0
+    sv = np.array([float(x) for x in capsys.readouterr().out.split()])
+    a = oracle.random_symmetric(3, 12)
+    mags = oracle.all_magnitudes(a).reshape(12, 12)[:, 4]
+    want = oracle.recover_signs(a, 4, mags, oracle.eigenvalues(a)[4])
+    assert sv.shape == (12,) and np.max(np.abs(sv - want)) <= 1e-9
     csv = tmp_path / "h.csv"
     csv.write_text("2,1\n1,2\n")
     assert cli.main(["component", "-i", "0", "-j", "1", "--csv", str(csv)]) == 0
