@@ -16,14 +16,16 @@
 // sweep s-1 has finished step k+1 (k+2 before prefetching step k+1), tracked
 // by per-warp progress counters in shared memory.  The leading sweep pulls
 // each block from HBM and the following sweeps re-read it from L2/L1, so
-// band traffic to HBM drops ~8x versus independent solves per warp (12
-// warps measured slower: 168 registers per thread and a smaller L1).  Within
-// a sweep a step never reads what the previous step wrote, so the blocks of
-// step k+1 are prefetched by cp.async while step k computes: the lower
-// triangle of D (packed) into a double buffer, C into sC as soon as step k
-// has read its rows (the left-apply's column sums are a shuffle butterfly,
-// not a shared-memory transpose).
-// CTAs pull solves from an atomic work counter (persistent kernel).
+// band traffic to HBM drops ~8x versus independent solves per warp.  One
+// CTA per SM: the followers' re-reads need a large L1, so shared memory is
+// kept to 13.4 KB per warp (two CTAs per SM — 16 warps at <= 128 registers —
+// measured 2.1x slower: the L1 shrinks to ~30 KB and the re-reads go to L2).
+// Within a sweep a step never reads what the previous step wrote, so the
+// blocks of step k+1 are prefetched by cp.async while step k computes: C into
+// sC once step k has taken its column sums from it, the packed lower
+// triangle of D into sD once step k's two-sided update has read D into
+// registers.  The left-apply's column sums come from the staged (not yet
+// right-applied) C: C1^T v2 = C^T v2 - (y . v2) v1 for C1 = C - y v1^T.
 #include "kernels.cuh"
 
 namespace eigenid_b200 {
@@ -37,7 +39,11 @@ constexpr int kWarpsPerCta = EIGENID_BULGE_WARPS;
 constexpr int kSLD = kCB + 1;
 constexpr int kBlk = kCB * kSLD;
 constexpr int kDP = kCB * (kCB + 1) / 2;        // packed lower triangle of D
-constexpr int kWarpSmem = kBlk + 2 * kDP + 3 * kCB;  // sC, sD[2], v, v2, w
+constexpr int kWarpSmem = kBlk + kDP + 3 * kCB;  // sC, sD, v, v2, w
+#ifndef EIGENID_BULGE_CTAS
+#define EIGENID_BULGE_CTAS 1
+#endif
+constexpr int kBulgeCtasPerSm = EIGENID_BULGE_CTAS;
 
 // Row-packed lower triangle: (r, c), r >= c.
 __device__ __forceinline__ int dp(int r, int c) { return (r * (r + 1) >> 1) + c; }
@@ -116,19 +122,47 @@ __device__ __forceinline__ double warp_householder(double x, int L, double* sv,
   return tau;
 }
 
+__device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
+                                           int L) {
+  // lower triangle of the L x L block: element (r, c), r >= c, lives at
+  // column c, diagonal r - c of the band (one coalesced run per column);
+  // out-of-range entries are zero-filled
+  const int lane = threadIdx.x & 31;
+  const double* base = AB + (long long)R * kCLD + lane;
+  if (L == kCB) {
+    cpa_tri_full<0>((unsigned)__cvta_generic_to_shared(sD + dp(lane, 0)), base, lane);
+    cpa_commit2();
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) {
+    if (lane >= c) {
+      const bool ok = lane < L;
+      cpa8(sD + dp(lane, c), ok ? base + c * (kCLD - 1) : AB, ok);
+    }
+  }
+  cpa_commit2();
+}
+
 // D <- H D H on the L x L diagonal block whose lower triangle is held in sD
 // (filled by cp.async; rows/cols >= L are zero; the upper triangle is read
-// through the mirror).  Writes the lower triangle back to the band.
+// through the mirror).  Writes the lower triangle back to the band.  Once D
+// is in registers, the next step's diagonal block (rows/cols nR.., nL of
+// them; nL = 0: none) is prefetched into the same buffer.
 template <bool FULL>
 __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
                                                 double tau, double* sw, int L,
-                                                double* AB, int R) {
+                                                double* AB, int R, int nR, int nL) {
   const int lane = threadIdx.x & 31;
   double drow[kCB];
   double pp[4] = {0.0, 0.0, 0.0, 0.0};
   const double2* v2 = reinterpret_cast<const double2*>(sv);
 #pragma unroll
   for (int c = 0; c < kCB; ++c) drow[c] = sD[c <= lane ? dp(lane, c) : dp(c, lane)];
+  if (nL > 0) {
+    __syncwarp();  // every lane has read its D row
+    prefetch_d(sD, AB, nR, nL);
+  }
 #pragma unroll
   for (int h = 0; h < kCB / 2; ++h) {  // broadcast reads, two per LDS.128
     const double2 v = v2[h];
@@ -159,28 +193,6 @@ __device__ __forceinline__ void two_sided_store(double* sD, const double* sv,
       st_pred(base + c * (kCLD - 1), drow[c], lane >= c && lane < L);
   }
   __syncwarp();
-}
-
-__device__ __forceinline__ void prefetch_d(double* sD, const double* AB, int R,
-                                           int L) {
-  // lower triangle of the L x L block: element (r, c), r >= c, lives at
-  // column c, diagonal r - c of the band (one coalesced run per column);
-  // out-of-range entries are zero-filled
-  const int lane = threadIdx.x & 31;
-  const double* base = AB + (long long)R * kCLD + lane;
-  if (L == kCB) {
-    cpa_tri_full<0>((unsigned)__cvta_generic_to_shared(sD + dp(lane, 0)), base, lane);
-    cpa_commit2();
-    return;
-  }
-#pragma unroll
-  for (int c = 0; c < kCB; ++c) {
-    if (lane >= c) {
-      const bool ok = lane < L;
-      cpa8(sD + dp(lane, c), ok ? base + c * (kCLD - 1) : AB, ok);
-    }
-  }
-  cpa_commit2();
 }
 
 // C = A[R1.., R..] (L1 x L) into sC (row r = lane, padded rows); one
@@ -241,7 +253,7 @@ __device__ __forceinline__ void publish(volatile long long* prog, int warp,
   if ((threadIdx.x & 31) == 0) prog[warp] = spos(s, k);
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 1)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, kBulgeCtasPerSm)
 bulge_chase_kernel(Stage2Args a) {
 #ifdef EIGENID_PHASE_TIMING
   long long t_b_ = clock64();
@@ -251,8 +263,8 @@ bulge_chase_kernel(Stage2Args a) {
   __shared__ int s_sidx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sC = smem + warp * kWarpSmem;
-  double* const sD0 = sC + kBlk;  // D double buffer: sD0 + buf * kDP
-  double* sv = sC + kBlk + 2 * kDP;
+  double* const sD = sC + kBlk;
+  double* sv = sD + kDP;
   double* sv2 = sv + kCB;
   double* sw = sv2 + kCB;
 
@@ -275,22 +287,19 @@ bulge_chase_kernel(Stage2Args a) {
       // block 0 and the prefetch of step 1 need sweep st-1 past step 2
       wait_prev(prog, warp, st, 2);
       const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
-      prefetch_d(sD0, AB, R0, L0);
-      if (have) {
-        prefetch_d(sD0 + kDP, AB, Rk, Lk);
-        prefetch_c(sC, AB, Rk, Lk, R0, L0);
-      }
+      prefetch_d(sD, AB, R0, L0);
+      if (have) prefetch_c(sC, AB, Rk, Lk, R0, L0);
       double beta;
       double tau = warp_householder(x, L0, sv, &beta);
       if (lane < L0) AB[(long long)st * kCLD + 1 + lane] = (lane == 0) ? beta : 0.0;
       cpa_wait_all();
       __syncwarp();
       if (L0 == kCB)
-        two_sided_store<true>(sD0, sv, tau, sw, L0, AB, R0);
+        two_sided_store<true>(sD, sv, tau, sw, L0, AB, R0, Rk, Lk);
       else
-        two_sided_store<false>(sD0, sv, tau, sw, L0, AB, R0);
+        two_sided_store<false>(sD, sv, tau, sw, L0, AB, R0, Rk, Lk);
       publish(prog, warp, st, 0);
-      int R = R0, L = L0, buf = 1, k = 1;
+      int R = R0, L = L0, k = 1;
       while (have) {
         // ---- step k on C = A[Rk.., R..] (Lk x L), D = A[Rk.., Rk..]; both
         // were prefetched during step k-1
@@ -303,13 +312,8 @@ bulge_chase_kernel(Stage2Args a) {
         const bool haven = Rn <= m - 1;
         const int Ln = haven ? min(kCB, m - Rn) : 0;
         BPH(0);
-        if (haven) {
-          wait_prev(prog, warp, st, k + 2);
-          BPH(6);
-          prefetch_d(sD0 + (buf ^ 1) * kDP, AB, Rn, Ln);
-          __syncwarp();  // every lane has read its C row from sC
-          prefetch_c(sC, AB, Rn, Ln, Rk, Lk);
-        }
+        if (haven) wait_prev(prog, warp, st, k + 2);  // before step k+1's prefetches
+        BPH(6);
         BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
         const double2* v2 = reinterpret_cast<const double2*>(sv);
@@ -332,31 +336,24 @@ bulge_chase_kernel(Stage2Args a) {
         const double tau2 = warp_householder(crow[0], Lk, sv2, &beta2);
         crow[0] = (lane == 0) ? beta2 : 0.0;
         BPH(2);
-        // left-apply to columns 1..L-1: w_c = tau2 sum_r v2_r C[r][c], the
-        // column sums by a butterfly reduce-scatter over the lanes (after
-        // round o, a lane holds partial sums for the half of its columns
-        // selected by lane bit o; lane c ends with column c)
+        // left-apply to columns 1..L-1: w_c = tau2 sum_r v2_r C1[r][c] with
+        // C1 = C - y v^T, i.e. tau2 ((C^T v2)_c - (y . v2) v_c); lane c takes
+        // column c of the staged C (conflict-free row reads)
         {
-          const double vr2 = sv2[lane];
-          double ps[kCB / 2];
+          const double2* u2 = reinterpret_cast<const double2*>(sv2);
+          double cc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < kCB / 2; ++j) {
-            const bool up = lane & 16;
-            const double send = vr2 * (up ? crow[j] : crow[j + 16]);
-            const double keep = vr2 * (up ? crow[j + 16] : crow[j]);
-            ps[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+          for (int h = 0; h < kCB / 2; ++h) {
+            const double2 u = u2[h];
+            cc[(2 * h) & 3] += sC[(2 * h) * kSLD + lane] * u.x;
+            cc[(2 * h + 1) & 3] += sC[(2 * h + 1) * kSLD + lane] * u.y;
           }
-#pragma unroll
-          for (int o = 8; o >= 1; o >>= 1) {
-#pragma unroll
-            for (int j = 0; j < o; ++j) {
-              const bool up = lane & o;
-              const double send = up ? ps[j] : ps[j + o];
-              const double keep = up ? ps[j + o] : ps[j];
-              ps[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-          }
-          sw[lane] = (lane >= 1 && lane < L) ? tau2 * ps[0] : 0.0;
+          const double yv = warp_sum(y * sv2[lane]);
+          const double cs = (cc[0] + cc[1]) + (cc[2] + cc[3]);
+          const double w = tau2 * (cs - yv * sv[lane]);
+          __syncwarp();  // every lane is done with sC and sw
+          if (haven) prefetch_c(sC, AB, Rn, Ln, Rk, Lk);
+          sw[lane] = (lane >= 1 && lane < L) ? w : 0.0;
         }
         __syncwarp();
         {
@@ -383,9 +380,9 @@ bulge_chase_kernel(Stage2Args a) {
         BPH(3);
         BPH(4);
         if (Lk == kCB)
-          two_sided_store<true>(sD0 + buf * kDP, sv2, tau2, sw, Lk, AB, Rk);
+          two_sided_store<true>(sD, sv2, tau2, sw, Lk, AB, Rk, Rn, Ln);
         else
-          two_sided_store<false>(sD0 + buf * kDP, sv2, tau2, sw, Lk, AB, Rk);
+          two_sided_store<false>(sD, sv2, tau2, sw, Lk, AB, Rk, Rn, Ln);
         BPH(5);
         sv[lane] = sv2[lane];
         publish(prog, warp, st, k);
@@ -395,7 +392,6 @@ bulge_chase_kernel(Stage2Args a) {
         Rk = Rn;
         Lk = Ln;
         have = haven;
-        buf ^= 1;
         ++k;
       }
       publish(prog, warp, st, 65535);  // sweep done
@@ -430,7 +426,8 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = a.nsolves < sms ? a.nsolves : sms;
+  const int slots = sms * kBulgeCtasPerSm;
+  const int grid = a.nsolves < slots ? a.nsolves : slots;
   bulge_chase_kernel<<<grid, kWarpsPerCta * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
