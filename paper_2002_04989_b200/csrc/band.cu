@@ -19,6 +19,8 @@
 // diagonals ready for the chase.
 #include "kernels.cuh"
 
+#include <type_traits>
+
 namespace eigenid_b200 {
 
 constexpr int kB = 32;      // bandwidth / panel width
@@ -56,6 +58,7 @@ constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
 // Fused pass (rest of panel p's update + SYMM of panel p+1): kFS stages of
 // {Bop rows, C tile, VT(cb) rows} plus the row block's VT(rb) rows.
 constexpr int kFVLD = 34, kFVRLD = 36;
+
 constexpr int kFSt = kG2N * kG2K + kG2M * kG2N + kB * kFVLD;
 constexpr int kFSmem = kFS * kFSt + kG2M * kFVRLD;
 constexpr int kGemmSmem =
@@ -877,10 +880,10 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     }
 #pragma unroll
     for (int p = 0; p < kFS - 1; ++p) stage(p);
-    for (int ci = 0; ci < ncb; ++ci) {
-      cpa_wait<kFS - 2>();
-      __syncthreads();
-      stage(ci + kFS - 1);
+    // Tile body, specialised on whether the tile may cross the diagonal
+    // (only then are the triangular masks needed).
+    auto tile = [&](int ci, auto diag_tag) {
+      constexpr bool diag = decltype(diag_tag)::value;
       const int cb = ci * kG2N;
       const double* b = sm + (ci % kFS) * kFSt;
       double* cs = const_cast<double*>(b) + kG2N * kG2K;
@@ -926,7 +929,6 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
       }
-      const bool diag = cb + kB > rb;  // the tile may cross the diagonal
       // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators: the
       // m8n8k4 accumulator of column tile q holds C[row][8q+2kk .. +1], which
       // is exactly this lane's A-fragment pair for k-pair q (no shared-memory
@@ -947,19 +949,24 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], ay, b1[nt]);
       }
+      auto store_c = [&]() {
 #pragma unroll
-      for (int nt = 0; nt < kG2N / 8; ++nt) {
-        const int col = cb + 8 * nt + 2 * kk;
-        if (r < sn) {
-          double* p = A22n + (long long)r * ldw + col;
-          if (col + 1 < sn)
-            *reinterpret_cast<double2*>(p) = make_double2(acc[nt][0], acc[nt][1]);
-          else if (col < sn)
-            p[0] = acc[nt][0];
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          const int col = cb + 8 * nt + 2 * kk;
+          if (r < sn) {
+            double* p = A22n + (long long)r * ldw + col;
+            if (col + 1 < sn)
+              *reinterpret_cast<double2*>(p) = make_double2(acc[nt][0], acc[nt][1]);
+            else if (col < sn)
+              p[0] = acc[nt][0];
+          }
         }
+      };
+      store_c();
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt)
         *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
             make_double2(acc[nt][0], acc[nt][1]);
-      }
       __syncthreads();
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 8*kXT cols)
       {
@@ -980,6 +987,15 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                 make_double2(x2[u][0], x2[u][1]);
         }
       }
+    };
+    for (int ci = 0; ci < ncb; ++ci) {
+      cpa_wait<kFS - 2>();
+      __syncthreads();
+      stage(ci + kFS - 1);
+      if (ci * kG2N + kB > rb)
+        tile(ci, std::true_type{});
+      else
+        tile(ci, std::false_type{});
     }
     // X[rb] += the row-part accumulators (after this row block's transposed
     // contributions to the same rows)
@@ -1151,7 +1167,7 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
     if (m - kB >= 2) {
       int par = 0;
       factor(0, m - kB, Vg[0], Xg[0]);
-      PHASE(4);
+      PHASE(7);
       gemm1(W + (long long)kB * ldw + kB, ldw, m - kB, VTg, Xg[0], sgemm);
       form_w2(m - kB, Vg[0], Xg[0]);
       for (;;) {
@@ -1161,7 +1177,7 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
         PHASE(6);
         if (s1 < 2) {
           gemm2(A22, ldw, s, Xg[par], Vg[par], sgemm);         // last update
-          PHASE(7);
+          PHASE(0);
           c += kB;
           break;
         }

@@ -18,7 +18,7 @@ eng = IdentityEngine()
 lam, mu = eng.minor_spectra(a, 0, rows)
 buf = (ctypes.c_ulonglong * 16)()
 lib.eigenid_debug_phase_cycles(buf)
-names = ['other', 'copy', 'panel', 'band+VT', 'gemm1', 'Y,M,W2', 'gemm2', '-']
+names = ['other', 'copy', 'panel', 'band+VT', 'fused', 'Y,M,W2', 'gemm2', 'gemm1']
 tot = sum(buf[i] for i in range(8))
 g1 = min(rows + 1, int(os.environ.get('SLOTS', '296')))
 print(f'stage 1 (summed over {g1} CTAs, shown per CTA):')
