@@ -14,6 +14,10 @@
 namespace eigenid_b200 {
 
 constexpr int kBisNT = 256;
+// Three CTAs per SM (64 KB of (d, e^2) each at m = 4095; <= 85 registers).
+// Two eigenvalues in flight per thread (two interleaved Sturm chains) measured
+// 29 % slower: the recurrence is issue-bound, not latency-bound.
+constexpr int kBisMinBlocks = 3;  // eigenvalues in flight per thread
 
 __device__ double block_reduce_max(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -30,7 +34,125 @@ __device__ double block_reduce_min(double v, double* red) {
   return -block_reduce_max(-v, red);
 }
 
-__global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
+// One eigenvalue's bracketing / secant state machine (see bisect_kernel).
+struct BisectLane {
+  int k = 0;
+  bool active = false, gersh = false;
+  int stage = 0, it = 0, side = 0, clo = 0, chi = 0, elo = 0, ehi = 0;
+  double lo = 0.0, hi = 0.0, plo = 0.0, phi = 0.0, w1 = 0.0, w2 = 0.0;
+
+  __device__ __forceinline__ void start(const double* lam, double delta, double glo,
+                                        double ghi, double sc, double glo_s,
+                                        double ghi_s) {
+    stage = 0;
+    if (lam) {
+      gersh = false;
+      lo = fmax(lam[k] - delta, glo) * sc;
+      hi = fmin(lam[k + 1] + delta, ghi) * sc;
+    } else {
+      gersh = true;
+      lo = glo_s;
+      hi = ghi_s;
+    }
+  }
+  // Next evaluation point; an eigenvalue that has converged is written out
+  // and the slot moves on to k + stride (active is cleared past k1).
+  __device__ __forceinline__ double next_x(double atol, double* out, double sc, int stride,
+                                           int k1, const double* lam, double delta,
+                                           double glo, double ghi, double glo_s,
+                                           double ghi_s) {
+    double x = 0.0;
+    if (stage == 2) {
+      bool fin = false;
+      const double w = hi - lo;
+      const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
+      if (w <= tol || it >= 300) {
+        fin = true;
+      } else {
+        x = lo + 0.5 * w;
+        const bool slow = it >= 2 && w > 0.5 * w2;
+        if (clo == k && chi == k + 1 && !slow) {
+          const int de = ehi - elo;
+          double r = phi / plo;
+          r = de > 1000 ? -1e300 : (de < -1000 ? -1e-300 : scalbn(r, de));
+          const double xs = lo + w / (1.0 - r);
+          const double g = 0.5 * tol;
+          x = fmin(fmax(xs, lo + g), hi - g);
+          if (!(x > lo && x < hi)) x = lo + 0.5 * w;
+        } else {
+          side = 0;
+        }
+        w2 = w1;
+        w1 = w;
+        if (!(x > lo && x < hi)) fin = true;  // a few ulps wide
+      }
+      if (fin) {
+#ifdef EIGENID_BISECT_STATS
+        atomicAdd(&g_bis_hist[it < 63 ? it : 63], 1ull);
+#endif
+        out[k] = (lo + 0.5 * (hi - lo)) / sc;
+        k += stride;
+        active = k < k1;
+        if (active) {
+          start(lam, delta, glo, ghi, sc, glo_s, ghi_s);
+          x = lo;
+        }
+      }
+    } else {
+      x = stage == 0 ? lo : hi;
+    }
+    return x;
+  }
+  __device__ __forceinline__ void update(int cx, double px, int ex, double x, double glo_s,
+                                         double ghi_s) {
+    if (stage == 0) {
+      clo = cx;
+      plo = px;
+      elo = ex;
+      if (!gersh && !(cx <= k && lo < hi)) {
+        gersh = true;  // interlacing check failed: Gershgorin bracket
+        lo = glo_s;
+        hi = ghi_s;
+      } else {
+        stage = 1;
+      }
+    } else if (stage == 1) {
+      chi = cx;
+      phi = px;
+      ehi = ex;
+      if (!gersh && !(cx > k)) {
+        gersh = true;
+        lo = glo_s;
+        hi = ghi_s;
+        stage = 0;
+      } else {
+        stage = 2;
+        it = 0;
+        side = 0;
+        w1 = w2 = 0.0;
+      }
+    } else {
+      if (cx > k) {
+        hi = x;
+        phi = px;
+        ehi = ex;
+        chi = cx;
+        if (side == 1) plo *= 0.5;  // Illinois: retained end twice
+        side = 1;
+      } else {
+        lo = x;
+        plo = px;
+        elo = ex;
+        clo = cx;
+        if (side == -1) phi *= 0.5;
+        side = -1;
+      }
+      ++it;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kBisNT, kBisMinBlocks) bisect_kernel(BisectArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[kBisNT / 32];
   __shared__ int unsorted;
@@ -71,122 +193,27 @@ __global__ void __launch_bounds__(kBisNT) bisect_kernel(BisectArgs a) {
   const int per = (m + a.split - 1) / a.split;
   const int k0 = part * per, k1 = min(m, k0 + per);
   // Each thread owns eigenvalues k = k0 + tid, + kBisNT, ... and runs them as
-  // a state machine, one Sturm evaluation per round: bracket low end, high
-  // end, then safeguarded secant/bisection (the arithmetic of bisect_from).
-  // A lane whose eigenvalue converges starts its next one in the same round,
-  // so the warp's rounds follow the mean, not the maximum, evaluation count.
-  // The interlacing bracket (minors) is verified by the counts at both ends;
-  // if either check fails the lane restarts on the Gershgorin interval.
+  // a state machine (BisectLane), one Sturm evaluation per round: bracket low
+  // end, high end, then safeguarded secant/bisection (the arithmetic of
+  // bisect_from).  A lane whose eigenvalue converges starts its next one in the
+  // same round, so the warp's rounds follow the mean, not the maximum,
+  // evaluation count.  The interlacing bracket (minors) is verified by the
+  // counts at both ends; if either check fails the lane restarts on the
+  // Gershgorin interval.
   const double glo_s = glo * sc, ghi_s = ghi * sc;
-  int k = k0 + threadIdx.x;
-  bool active = k < k1;
-  bool gersh = false;
-  int stage = 0, it = 0, side = 0, clo = 0, chi = 0, elo = 0, ehi = 0;
-  double lo = 0.0, hi = 0.0, plo = 0.0, phi = 0.0, w1 = 0.0, w2 = 0.0;
-  auto start = [&]() {
-    stage = 0;
-    if (a.lam) {
-      gersh = false;
-      lo = fmax(a.lam[k] - delta, glo) * sc;
-      hi = fmin(a.lam[k + 1] + delta, ghi) * sc;
-    } else {
-      gersh = true;
-      lo = glo_s;
-      hi = ghi_s;
-    }
-  };
-  if (active) start();
-  while (__any_sync(0xffffffffu, active)) {
+  BisectLane ln;
+  ln.k = k0 + threadIdx.x;
+  ln.active = ln.k < k1;
+  if (ln.active) ln.start(a.lam, delta, glo, ghi, sc, glo_s, ghi_s);
+  while (__any_sync(0xffffffffu, ln.active)) {
     double x = 0.0;
-    if (active) {
-      if (stage == 2) {
-        bool fin = false;
-        const double w = hi - lo;
-        const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
-        if (w <= tol || it >= 300) {
-          fin = true;
-        } else {
-          x = lo + 0.5 * w;
-          const bool slow = it >= 2 && w > 0.5 * w2;
-          if (clo == k && chi == k + 1 && !slow) {
-            const int de = ehi - elo;
-            double r = phi / plo;
-            r = de > 1000 ? -1e300 : (de < -1000 ? -1e-300 : scalbn(r, de));
-            const double xs = lo + w / (1.0 - r);
-            const double g = 0.5 * tol;
-            x = fmin(fmax(xs, lo + g), hi - g);
-            if (!(x > lo && x < hi)) x = lo + 0.5 * w;
-          } else {
-            side = 0;
-          }
-          w2 = w1;
-          w1 = w;
-          if (!(x > lo && x < hi)) fin = true;  // a few ulps wide
-        }
-        if (fin) {
-#ifdef EIGENID_BISECT_STATS
-          atomicAdd(&g_bis_hist[it < 63 ? it : 63], 1ull);
-#endif
-          out[k] = (lo + 0.5 * (hi - lo)) / sc;
-          k += kBisNT;
-          active = k < k1;
-          if (active) {
-            start();
-            x = lo;
-          }
-        }
-      } else {
-        x = stage == 0 ? lo : hi;
-      }
-    }
-    if (active) {
+    if (ln.active)
+      x = ln.next_x(atol, out, sc, kBisNT, k1, a.lam, delta, glo, ghi, glo_s, ghi_s);
+    if (ln.active) {
       double px;
       int ex;
       const int cx = sturm_det(sd, se2, m, x, &px, &ex);
-      if (stage == 0) {
-        clo = cx;
-        plo = px;
-        elo = ex;
-        if (!gersh && !(cx <= k && lo < hi)) {
-          gersh = true;  // interlacing check failed: Gershgorin bracket
-          lo = glo_s;
-          hi = ghi_s;
-        } else {
-          stage = 1;
-        }
-      } else if (stage == 1) {
-        chi = cx;
-        phi = px;
-        ehi = ex;
-        if (!gersh && !(cx > k)) {
-          gersh = true;
-          lo = glo_s;
-          hi = ghi_s;
-          stage = 0;
-        } else {
-          stage = 2;
-          it = 0;
-          side = 0;
-          w1 = w2 = 0.0;
-        }
-      } else {
-        if (cx > k) {
-          hi = x;
-          phi = px;
-          ehi = ex;
-          chi = cx;
-          if (side == 1) plo *= 0.5;  // Illinois: retained end twice
-          side = 1;
-        } else {
-          lo = x;
-          plo = px;
-          elo = ex;
-          clo = cx;
-          if (side == -1) phi *= 0.5;
-          side = -1;
-        }
-        ++it;
-      }
+      ln.update(cx, px, ex, x, glo_s, ghi_s);
     }
   }
   if (a.split > 1) return;  // cross-CTA order is checked by sort_fix_kernel
