@@ -485,10 +485,10 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
         t1 = statistics.mean(stage1_ms) / 1e3
         achieved = f_tri(n, rows) / t1 / 1e12
         # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
-        # --set full capture of a 296-solve wave (profiles/
-        # r01c_band_4096_fused_raw_summary.csv: 2.851 TB read + 1.411 TB
+        # --set full capture of 296 solves (profiles/
+        # r01g_band_4096_wide_raw_summary.csv: 2.061 TB read + 1.231 TB
         # written), scaled to this launch's solve count
-        traffic = (2.851206e12 + 1.411389e12) / 296 * (rows + 1) if n == 4096 else None
+        traffic = (2.060936e12 + 1.231415e12) / 296 * (rows + 1) if n == 4096 else None
         roof = {"bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
                 "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": traffic,
