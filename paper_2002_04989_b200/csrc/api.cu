@@ -196,6 +196,9 @@ int begin(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
 // Per-stage device timing of run_large: enabled per context through
 // eigenid_gpu_set_profiling (bench.py reads it to time the stage-1 kernel on
 // its own stream) or EIGENID_PROFILE=1 (also printed to stderr).
+// Same-box A/B: the wide stage-1 layout wins at n = 4096, the
+// narrow one at n = 1024.
+constexpr int kStage1WideMinN = 3072;
 constexpr int kStages = 5;  // stage1, stage2, bisect_A, bisect_minors, identity
 struct StageTimer {
   bool on = false, print = false;
@@ -262,7 +265,10 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   const double solve_bytes = 8.0 * (band_stride + 3.0 * n);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  const int max_slots = sms * stage1_ctas_per_sm();
+  // Stage-1 layout (band.cu): wide (one 16-warp CTA per SM) for large n,
+  // narrow (two 8-warp CTAs per SM) where the panel phases weigh more.
+  const bool wide = n >= kStage1WideMinN;
+  const int max_slots = sms * (wide ? wide::stage1_ctas_per_sm() : narrow::stage1_ctas_per_sm());
   int slots = nsolves < max_slots ? nsolves : max_slots;
   while (slots > 1 && slots * ws_bytes > 0.7 * budget) slots = (slots + 1) / 2;
   long long chunk = (long long)((budget - slots * ws_bytes) / solve_bytes);
@@ -286,7 +292,9 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
     ++launches;
     Stage1Args s1{dA, n, djs, cnt, c->bWs.as<double>(), ws_stride, ldw,
                   c->bBand.as<double>(), band_stride, c->bCounter.as<int>() + 1};
-    EID_CUDA(launch_stage1(s1, cnt < slots ? cnt : slots, st), "stage1");
+    const int grid1 = cnt < slots ? cnt : slots;
+    EID_CUDA(wide ? wide::launch_stage1(s1, grid1, st) : narrow::launch_stage1(s1, grid1, st),
+             "stage1");
     ++launches;
     timer.mark(0);
     Stage2Args s2{c->bBand.as<double>(), band_stride, djs, cnt, n,

@@ -21,15 +21,22 @@
 
 #include <type_traits>
 
+#ifndef EIGENID_STAGE1_NS  // band_narrow.cu compiles this file again as "narrow"
+#define EIGENID_STAGE1_NS wide
+#define EIGENID_STAGE1_PRIMARY 1
+#endif
+
 namespace eigenid_b200 {
+namespace EIGENID_STAGE1_NS {
 
 constexpr int kB = 32;      // bandwidth / panel width
-// Two layouts: "wide" (default): 16 warps and one CTA per SM (128-row
-// blocks: half the Bop / VT / X re-reads per trailing element, three-stage
-// fused pipeline, half the workspace slots), or 8 warps and two CTAs per SM
-// (64-row blocks; the second CTA fills the DMMA pipe during panel phases).
-// Same-box A/B at n = 4096 (4096 minors): wide 0.6 % faster (3.3 % on
-// short runs that stay below the power cap).
+// Two layouts, both compiled (namespaces wide / narrow; api.cu picks by n):
+// "wide": 16 warps and one CTA per SM (128-row blocks: half the Bop / VT / X
+// re-reads per trailing element, three-stage fused pipeline, half the
+// workspace slots), or "narrow": 8 warps and two CTAs per SM (64-row
+// blocks; the second CTA fills the DMMA pipe during the other's panel
+// phases, which weigh more at small n).  Same-box A/B: wide 0.6 % faster at
+// n = 4096 (-23 % DRAM bytes), narrow 13 % faster at n = 1024.
 #ifndef EIGENID_STAGE1_WIDE
 #define EIGENID_STAGE1_WIDE 1
 #endif
@@ -1220,7 +1227,7 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
 #endif
 }
 
-#ifdef EIGENID_PHASE_TIMING
+#if defined(EIGENID_PHASE_TIMING) && defined(EIGENID_STAGE1_PRIMARY)
 extern "C" void eigenid_debug_phase_cycles(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
 }
@@ -1230,12 +1237,7 @@ extern "C" void eigenid_debug_cta_span(unsigned long long* out) {
 #endif
 
 size_t stage1_smem_bytes() { return sizeof(double) * (size_t)kStage1SmemDoubles; }
-int stage1_band_ld() { return kLDAB; }
-int stage1_bandwidth() { return kB; }
 int stage1_ctas_per_sm() { return kCtasPerSm; }
-long long stage1_ws_doubles(int n, int ldw) {
-  return (long long)n * ldw + 5LL * n * kB;
-}
 
 cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st) {
   const size_t smem = stage1_smem_bytes();
@@ -1247,5 +1249,17 @@ cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st) {
   band_reduce_kernel<<<grid, kNT, smem, st>>>(a);
   return cudaGetLastError();
 }
+
+}  // namespace EIGENID_STAGE1_NS
+
+#ifdef EIGENID_STAGE1_PRIMARY
+// layout-independent band / workspace geometry
+int stage1_band_ld() { return EIGENID_STAGE1_NS::kLDAB; }
+int stage1_bandwidth() { return EIGENID_STAGE1_NS::kB; }
+long long stage1_ws_doubles(int n, int ldw) {
+  return (long long)n * ldw + 5LL * n * EIGENID_STAGE1_NS::kB;
+}
+
+#endif
 
 }  // namespace eigenid_b200

@@ -30,11 +30,19 @@ struct Stage1Args {
   long long band_stride;
   int* counter;       // work queue (zeroed before launch)
 };
+// Two compiled layouts of the same kernel (band.cu header): wide (16 warps,
+// one CTA per SM) and narrow (8 warps, two CTAs per SM).
+namespace wide {
 cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
+int stage1_ctas_per_sm();
+}  // namespace wide
+namespace narrow {
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
+int stage1_ctas_per_sm();
+}  // namespace narrow
 int stage1_band_ld();
 int stage1_bandwidth();
 long long stage1_ws_doubles(int n, int ldw);  // per-slot workspace
-int stage1_ctas_per_sm();
 
 // ---- bulge.cu: stage 2, band -> tridiagonal
 struct Stage2Args {
