@@ -267,7 +267,12 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   // Stage-1 layout (band.cu): wide (one 16-warp CTA per SM) for large n,
   // narrow (two 8-warp CTAs per SM) where the panel phases weigh more.
-  const bool wide = n >= kStage1WideMinN;
+  bool wide = n >= kStage1WideMinN;
+  // EIGENID_STAGE1_LAYOUT=wide|narrow overrides the choice (tests, A/B).
+  if (const char* lay = std::getenv("EIGENID_STAGE1_LAYOUT")) {
+    if (std::strcmp(lay, "wide") == 0) wide = true;
+    if (std::strcmp(lay, "narrow") == 0) wide = false;
+  }
   const int max_slots = sms * (wide ? wide::stage1_ctas_per_sm() : narrow::stage1_ctas_per_sm());
   int slots = nsolves < max_slots ? nsolves : max_slots;
   while (slots > 1 && slots * ws_bytes > 0.7 * budget) slots = (slots + 1) / 2;

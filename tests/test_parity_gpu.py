@@ -181,6 +181,28 @@ def test_chunked_memory_plan_is_bit_identical(engine, oracle, monkeypatch):
     monkeypatch.delenv("EIGENID_MEM_BUDGET")
 
 
+@pytest.mark.parametrize("n", [300, 1031])
+def test_stage1_layouts_agree(engine, oracle, monkeypatch, n):
+    """Both compiled stage-1 layouts (wide: one 16-warp CTA per SM; narrow:
+    two 8-warp CTAs per SM) reduce the same minors; they differ only in the
+    rounding order of the trailing updates, so their spectra agree to a few
+    ulps of ||A|| and each matches the oracle."""
+    a = oracle.random_symmetric(5, n) * np.sqrt(2.0 / n)
+    rows = [0, n // 2, n - 1]
+    got = {}
+    for lay in ("wide", "narrow"):
+        monkeypatch.setenv("EIGENID_STAGE1_LAYOUT", lay)
+        got[lay] = engine.minor_spectra(a, 0, n)
+    monkeypatch.delenv("EIGENID_STAGE1_LAYOUT")
+    (lw, mw), (ln, mn) = got["wide"], got["narrow"]
+    assert np.max(np.abs(lw - ln)) <= 1e-13
+    assert np.max(np.abs(mw - mn)) <= 1e-13
+    for j in rows:
+        want = oracle.eigenvalues(oracle.minor(a, j))
+        assert np.max(np.abs(mw[j] - want)) <= 1e-13
+        assert np.max(np.abs(mn[j] - want)) <= 1e-13
+
+
 # ------------------------------------------------------------- configs
 def test_c1_n64(engine, oracle, gold):
     a = oracle.random_symmetric(1, 64)
