@@ -80,14 +80,37 @@ __device__ __forceinline__ int sturm_det(const double* __restrict__ d,
   int ex = 0;
   int k = 1;
   for (; k + 4 <= m; k += 4) {
+    // Fast path: four steps without the zero fix-up, tracking whether any
+    // p came out exactly zero (integer min of the magnitude bits); in that
+    // rare case the block is recomputed with the fix-up, so the result is
+    // bit-identical to applying it at every step.
+    double q0 = p0, q1 = p1;
+    int c = cnt;
+    unsigned nz = 0xffffffffu;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      double p2 = fma(d[k + u] - x, p1, -e2[k + u - 1] * p0);
-      if (is_zero_bits(p2)) p2 = -p1 * 0x1p-900;
-      cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
-      p0 = p1;
-      p1 = p2;
+      const double p2 = fma(d[k + u] - x, q1, -e2[k + u - 1] * q0);
+      nz = min(nz, (unsigned)((__double2hiint(p2) & 0x7fffffff) | __double2loint(p2)));
+      c += (__double2hiint(p2) ^ __double2hiint(q1)) < 0;
+      q0 = q1;
+      q1 = p2;
     }
+    if (nz == 0u) {
+      q0 = p0;
+      q1 = p1;
+      c = cnt;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double p2 = fma(d[k + u] - x, q1, -e2[k + u - 1] * q0);
+        if (is_zero_bits(p2)) p2 = -q1 * 0x1p-900;
+        c += (__double2hiint(p2) ^ __double2hiint(q1)) < 0;
+        q0 = q1;
+        q1 = p2;
+      }
+    }
+    p0 = q0;
+    p1 = q1;
+    cnt = c;
     // renormalise by a power of two when the larger exponent leaves
     // [2^-256, 2^256] (integer test on the exponent fields)
     const int eb = max(biased_exp(p0), biased_exp(p1));
