@@ -117,6 +117,25 @@ def test_hand_cases_and_errors(engine, gold):
         engine.all_magnitudes(np.eye(1))
 
 
+@pytest.mark.parametrize("n", [40, 100, 300])
+def test_exact_zero_sturm_pivots(engine, oracle, n):
+    """Integer diagonal (and block-diagonal) matrices: the tridiagonals have
+    exact zeros off the diagonal, so Sturm evaluations at integer points hit
+    exactly-zero pivots (the recurrence's zero fix-up path).  |v_ij|^2 of a
+    diagonal matrix is a permutation matrix; the block case is checked
+    against the oracle."""
+    rng = np.random.default_rng(n)
+    d = rng.permutation(n).astype(np.float64) + 1.0
+    g = engine.all_magnitudes(np.diag(d)).reshape(n, n)
+    want = (d[:, None] == np.sort(d)[None, :]).astype(np.float64)  # out[j][i]
+    assert np.max(np.abs(g - want)) <= 1e-12
+    a = np.diag(2.0 * d)
+    for k in range(0, n - 1, 4):  # 2 x 2 blocks among exact diagonal entries
+        a[k, k + 1] = a[k + 1, k] = 1.0
+    g = engine.all_magnitudes(a).reshape(n, n)
+    assert mixed_ok(g, np.asarray(oracle.all_magnitudes(a)).reshape(n, n), abs_=1e-12)
+
+
 def test_solve_count_contract(oracle):
     from paper_2002_04989_b200 import IdentityEngine
     eng = IdentityEngine()
