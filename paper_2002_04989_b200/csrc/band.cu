@@ -32,8 +32,7 @@ namespace EIGENID_STAGE1_NS {
 constexpr int kB = 32;      // bandwidth / panel width
 // Two layouts, both compiled (namespaces wide / narrow; api.cu picks by n):
 // "wide": 16 warps and one CTA per SM (128-row blocks: half the Bop / VT / X
-// re-reads per trailing element, three-stage fused pipeline, half the
-// workspace slots), or "narrow": 8 warps and two CTAs per SM (64-row
+// re-reads per trailing element, half the workspace slots), or "narrow": 8 warps and two CTAs per SM (64-row
 // blocks; the second CTA fills the DMMA pipe during the other's panel
 // phases, which weigh more at small n).  Same-box A/B: wide 0.6 % faster at
 // n = 4096 (-23 % DRAM bytes), narrow 13 % faster at n = 1024.
@@ -59,7 +58,12 @@ constexpr int kGramPart = 8 * kSmallMat;             // 8 partial Gram slots
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int kG1S = 3;                             // GEMM 1 cp.async stages
 constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
-constexpr int kFS = EIGENID_STAGE1_WIDE ? 3 : 2;      // fused-pass stages
+// Fused-pass cp.async stages: two in both layouts (a third stage in the wide
+// layout measured 1.1 % slower at n = 4096: 58 KB less L1).
+#ifndef EIGENID_FUSED_STAGES
+#define EIGENID_FUSED_STAGES 2
+#endif
+constexpr int kFS = EIGENID_FUSED_STAGES;            // fused-pass stages
 constexpr int kXT = 16 / kNW;  // 8x8 tiles of the fused transposed product per warp
 constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
 #ifndef EIGENID_STAGE1_FUSED
