@@ -11,12 +11,13 @@
 // position, so a step touches only C and D (band storage keeps 2kB+1
 // diagonals per column).
 //
-// A CTA owns one solve at a time and its 8 warps chase 8 consecutive
-// sweeps concurrently (warp w takes sweeps w, w+8, ...): sweep s may run step k once
-// sweep s-1 has finished step k+1 (k+2 before prefetching step k+1), tracked
-// by per-warp progress counters in shared memory.  The leading sweep pulls
-// each block from HBM and the following sweeps re-read it from L2/L1, so
-// band traffic to HBM drops ~8x versus independent solves per warp.  One
+// A CTA owns one solve at a time and its warps (nine) chase as many
+// consecutive sweeps concurrently (warp w takes sweeps w, w + 9, ...): sweep
+// s may run step k once sweep s-1 has finished step k+1 (k+2 before
+// prefetching step k+1), tracked by per-warp progress counters in shared
+// memory.  The leading sweep pulls each block from HBM and the following
+// sweeps re-read it from L2/L1, so band traffic to HBM drops ~9x versus
+// independent solves per warp.  One
 // CTA per SM: the followers' re-reads need a large L1, so shared memory is
 // kept to 13.4 KB per warp (two CTAs per SM — 16 warps at <= 128 registers —
 // measured 2.1x slower: the L1 shrinks to ~30 KB and the re-reads go to L2).
@@ -32,10 +33,13 @@ namespace eigenid_b200 {
 
 constexpr int kCB = 32;              // bandwidth (must match band.cu kB)
 constexpr int kCLD = 2 * kCB + 1;    // band diagonals stored per column
-#ifndef EIGENID_BULGE_WARPS
-#define EIGENID_BULGE_WARPS 8
-#endif
-constexpr int kWarpsPerCta = EIGENID_BULGE_WARPS;
+// Warps (= sweeps in flight per solve) per CTA, by matrix size: nine for
+// long sweeps (one SM sub-partition then holds three warps, so the register
+// cap is 168 with small spills, and it still measured 1.1 % faster than
+// eight at n = 4096), eight below (nine is 6 % slower at n = 1024); ten or
+// more are slower everywhere.
+constexpr int kWarpsLong = 9, kWarpsShort = 8;
+constexpr int kWarpsLongMinN = 3072;
 constexpr int kSLD = kCB + 1;
 constexpr int kBlk = kCB * kSLD;
 constexpr int kDP = kCB * (kCB + 1) / 2;        // packed lower triangle of D
@@ -233,12 +237,12 @@ __device__ __forceinline__ long long spos(int sweep, int step) {
   return (long long)sweep * 65536 + step;
 }
 
-// Blocks until sweep s-1 (owned by warp w-1 mod kWarpsPerCta) has finished
-// step k.
+// Blocks until sweep s-1 (owned by warp w-1 mod W) has finished step k.
+template <int W>
 __device__ __forceinline__ void wait_prev(volatile long long* prog, int warp,
                                           int s, int k) {
   if (s == 0) return;
-  const int pw = (warp + kWarpsPerCta - 1) % kWarpsPerCta;
+  const int pw = (warp + W - 1) % W;
   const long long need = spos(s - 1, k);
   if ((threadIdx.x & 31) == 0)
     while (prog[pw] < need) __nanosleep(64);
@@ -253,6 +257,7 @@ __device__ __forceinline__ void publish(volatile long long* prog, int warp,
   if ((threadIdx.x & 31) == 0) prog[warp] = spos(s, k);
 }
 
+template <int kWarpsPerCta>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, kBulgeCtasPerSm)
 bulge_chase_kernel(Stage2Args a) {
 #ifdef EIGENID_PHASE_TIMING
@@ -285,7 +290,7 @@ bulge_chase_kernel(Stage2Args a) {
       bool have = Rk <= m - 1;
       int Lk = have ? min(kCB, m - Rk) : 0;
       // block 0 and the prefetch of step 1 need sweep st-1 past step 2
-      wait_prev(prog, warp, st, 2);
+      wait_prev<kWarpsPerCta>(prog, warp, st, 2);
       const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
       prefetch_d(sD, AB, R0, L0);
       if (have) prefetch_c(sC, AB, Rk, Lk, R0, L0);
@@ -312,7 +317,7 @@ bulge_chase_kernel(Stage2Args a) {
         const bool haven = Rn <= m - 1;
         const int Ln = haven ? min(kCB, m - Rn) : 0;
         BPH(0);
-        if (haven) wait_prev(prog, warp, st, k + 2);  // before step k+1's prefetches
+        if (haven) wait_prev<kWarpsPerCta>(prog, warp, st, k + 2);  // before step k+1's prefetches
         BPH(6);
         BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T
@@ -417,19 +422,26 @@ extern "C" void eigenid_debug_bulge_cycles(unsigned long long* out) {
 }
 #endif
 
-cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
-  const size_t smem = sizeof(double) * kWarpSmem * kWarpsPerCta;
+template <int W>
+static cudaError_t launch_chase(const Stage2Args& a, int grid, cudaStream_t st) {
+  const size_t smem = sizeof(double) * kWarpSmem * W;
   cudaError_t e = cudaFuncSetAttribute(
-      bulge_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      bulge_chase_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  bulge_chase_kernel<W><<<grid, W * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
+  cudaError_t e;
   e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int slots = sms * kBulgeCtasPerSm;
   const int grid = a.nsolves < slots ? a.nsolves : slots;
-  bulge_chase_kernel<<<grid, kWarpsPerCta * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  return a.n >= kWarpsLongMinN ? launch_chase<kWarpsLong>(a, grid, st)
+                               : launch_chase<kWarpsShort>(a, grid, st);
 }
 
 }  // namespace eigenid_b200
