@@ -486,9 +486,9 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
         achieved = f_tri(n, rows) / t1 / 1e12
         # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
         # --set full capture of 296 solves (profiles/
-        # r01g_band_4096_wide_raw_summary.csv: 2.061 TB read + 1.231 TB
+        # r01h_band_4096_wide_raw_summary.csv: 2.053 TB read + 1.231 TB
         # written), scaled to this launch's solve count
-        traffic = (2.060936e12 + 1.231415e12) / 296 * (rows + 1) if n == 4096 else None
+        traffic = (2.052512e12 + 1.230878e12) / 296 * (rows + 1) if n == 4096 else None
         roof = {"bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
                 "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": traffic,
