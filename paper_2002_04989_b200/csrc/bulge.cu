@@ -29,6 +29,8 @@
 // right-applied) C: C1^T v2 = C^T v2 - (y . v2) v1 for C1 = C - y v1^T.
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace eigenid_b200 {
 
 constexpr int kCB = 32;              // bandwidth (must match band.cu kB)
@@ -440,8 +442,14 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int slots = sms * kBulgeCtasPerSm;
   const int grid = a.nsolves < slots ? a.nsolves : slots;
-  return a.n >= kWarpsLongMinN ? launch_chase<kWarpsLong>(a, grid, st)
-                               : launch_chase<kWarpsShort>(a, grid, st);
+  bool long_sweeps = a.n >= kWarpsLongMinN;
+  // EIGENID_STAGE2_WARPS=8|9 overrides the size-based choice (tests, A/B).
+  if (const char* w = std::getenv("EIGENID_STAGE2_WARPS")) {
+    if (w[0] == '8') long_sweeps = false;
+    if (w[0] == '9') long_sweeps = true;
+  }
+  return long_sweeps ? launch_chase<kWarpsLong>(a, grid, st)
+                     : launch_chase<kWarpsShort>(a, grid, st);
 }
 
 }  // namespace eigenid_b200

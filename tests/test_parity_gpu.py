@@ -222,6 +222,21 @@ def test_stage1_layouts_agree(engine, oracle, monkeypatch, n):
         assert np.max(np.abs(mn[j] - want)) <= 1e-13
 
 
+def test_stage2_warp_counts_bit_identical(engine, oracle, monkeypatch):
+    """The bulge chase runs W sweeps in flight per solve (8 or 9 warps by
+    size); every sweep's arithmetic is the same whichever warp runs it, so
+    the tridiagonals and spectra must agree bit for bit."""
+    n = 300
+    a = oracle.random_symmetric(11, n) * np.sqrt(2.0 / n)
+    got = {}
+    for w in ("8", "9"):
+        monkeypatch.setenv("EIGENID_STAGE2_WARPS", w)
+        got[w] = engine.minor_spectra(a, 0, n)
+    monkeypatch.delenv("EIGENID_STAGE2_WARPS")
+    for x, y in zip(got["8"], got["9"]):
+        assert np.array_equal(bits(x), bits(y))
+
+
 # ------------------------------------------------------------- configs
 def test_c1_n64(engine, oracle, gold):
     a = oracle.random_symmetric(1, 64)
