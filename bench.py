@@ -1,25 +1,33 @@
 #!/usr/bin/env python
-"""bench.py — headline benchmark of the B200 eigenvector–eigenvalue identity.
+"""bench.py — benchmark of the B200 eigenvector–eigenvalue identity.
 
-Default workload (BASELINE.json metric "|v_ij|^2 components/sec + % FP64 peak;
-end-to-end n=4096 time at 1/2/4/8 GPUs"): config C4, the full all_magnitudes
-pipeline (identity.cpp:294-316) on one n = 4096 GOE matrix
+Headline workload (BASELINE.json metric "|v_ij|^2 components/sec + % FP64
+peak; end-to-end n=4096 time at 1/2/4/8 GPUs"): config C4, the full
+all_magnitudes pipeline (identity.cpp:294-316) on one n = 4096 GOE matrix
 A = (G + G^T)/sqrt(2n) (random_symmetric(42, 4096).scaled(sqrt(2/4096))),
 i.e. lambda(A) + 4096 minor spectra + the 4096^2 identity products.  Under
 torchrun the minor index j is sharded over ranks (rank r owns rows
 [r n/N, (r+1) n/N) of out[j*n+i]); lambda(A) is recomputed per rank and the
 rows are all-gathered with NCCL (the path's only exchange).  Strong scaling.
 
+At N = 1 the same JSON line also carries `configs`: C1, C2, C3 and C5
+measured the same way (bounded step counts), each with its own e2e,
+cpu_baseline and parity record.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C1|C2|C3|C4|C5] [--no-cpu-baseline]
+                    [--config C1|C2|C3|C4|C5] [--no-cpu-baseline] [--no-subconfigs]
 
 Prints ONE JSON line on rank 0.  `value` is device-timed with CUDA events on
 the library's stream (inputs resident in HBM), max over ranks; `e2e` goes
-through the public API with host buffers (H2D of A and D2H of |v|^2 inside the
-timed region); `roofline` is the stage-1 band-reduction kernel (the dominant
-launch) against the measured FP64 DMMA peak; `cpu_baseline` times the oracle
-port on a bounded sample on this host.  --impl reference times the unmodified
-reference (oracle/_ref, compiled from /root/reference/proj/src) instead.
+through the public API with host buffers (H2D of the inputs and D2H of
+|v|^2 inside the timed region); `roofline` is the stage-1 band-reduction
+kernel (the dominant launch) against the measured FP64 DMMA peak;
+`cpu_baseline` times the oracle port on a bounded sample on this host and
+`parity` compares the GPU's output with the reference's committed goldens
+(tests/golden/reference_c{3,4}.npz, reference_golden.npz) or with the oracle
+on the cpu_baseline's own sample.  --impl reference times the unmodified
+reference (oracle/_ref, compiled from /root/reference/proj/src); its inputs
+come from oracle/_ref and the oracle, so no product library is loaded there.
 """
 from __future__ import annotations
 
@@ -37,11 +45,15 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 P_FP64_MEASURED_TFLOPS = 37.09   # tools/fp64_peak.cu DMMA m8n8k4 on this pool
-P_FP64_SOURCE = "measured: tools/fp64_peak.cu, DMMA m8n8k4 f64 (profiles/r01_fp64_peak.json)"
+P_FP64_SOURCE = ("measured: tools/fp64_peak.cu, DMMA m8n8k4 f64 "
+                 "(profiles/r01_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)")
 METRIC = "|v_ij|^2 components/sec"
 UNIT = "components/s"
+SUB_STEPS = {"C1": 20, "C2": 10, "C3": 5, "C4": 2, "C5": 2}
+C5_SEED = 5
 
 
 # ----------------------------------------------------------------- inputs
@@ -53,19 +65,9 @@ def goe_matrix(n: int, seed: int = 42) -> np.ndarray:
 
 
 def c3_matrix(n: int = 1024, seed: int = 3) -> np.ndarray:
-    """A = Q diag(linspace(-1,1)) Q^T, Q from QR of a seeded Gaussian, sign-fixed
-    by diag(R), then build(kSymmetrize)."""
-    from paper_2002_04989_b200.engine import seeded_draws
-    g = seeded_draws(seed, n * n).reshape(n, n)
-    q, r = np.linalg.qr(g)
-    q = q * np.sign(np.diag(r))[None, :]
-    lam = -1.0 + 2.0 * np.arange(n) / (n - 1)
-    a = (q * lam[None, :]) @ q.T
-    iu = np.triu_indices(n, 1)
-    mid = 0.5 * (a[iu] + a.T[iu])
-    a[iu] = mid
-    a.T[iu] = mid
-    return np.ascontiguousarray(a)
+    """Q diag(linspace(-1,1)) Q^T (product host generator)."""
+    from paper_2002_04989_b200 import c3_matrix as gen
+    return gen(n, seed)
 
 
 def f_tri(n: int, rows: int) -> float:
@@ -76,6 +78,30 @@ def f_tri(n: int, rows: int) -> float:
 def f_id(n: int, rows: int) -> float:
     """4 n (n-1) per row: identity-stage flops (identity.cpp:68,70,209-210)."""
     return 4.0 * rows * n * (n - 1)
+
+
+def f_chase(n: int, rows: int, b: int = 32) -> float:
+    """Bulge chase, ~6 b m^2 flops per solve (one Householder of length b per
+    step applied two-sided to a (b+1)-wide band window, m^2/b steps... per
+    DESIGN §4)."""
+    return 6.0 * b * (n ** 2 + rows * (n - 1) ** 2)
+
+
+# ----------------------------------------------------------------- parity
+def parity_record(g: np.ndarray, c: np.ndarray, checker: str, sample: str,
+                  rel: float = 1e-9, abs_: float = 1e-12) -> dict:
+    """SURVEY §8 d0 predicate |g - c| <= rel |c| + abs, plus max abs error and
+    max relative error on entries >= 1e-3."""
+    g = np.asarray(g, np.float64)
+    c = np.asarray(c, np.float64)
+    d = np.abs(g - c)
+    big = np.abs(c) >= 1e-3
+    return {"checker": checker, "sample": sample,
+            "predicate": f"|g-c| <= {rel:g}|c| + {abs_:g}",
+            "ok": bool(np.all(d <= rel * np.abs(c) + abs_)),
+            "max_abs": float(d.max()) if d.size else 0.0,
+            "max_rel_ge_1e-3": float((d[big] / np.abs(c[big])).max()) if big.any() else 0.0,
+            "bit_exact_frac": float(np.mean(g.view(np.uint64) == c.view(np.uint64)))}
 
 
 # ----------------------------------------------------------------- clocks
@@ -96,7 +122,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -174,18 +200,95 @@ class Dist:
             self.pg.destroy_process_group()
 
 
-# ----------------------------------------------------------------- CPU legs
-def cpu_baseline_c4(n: int, a: np.ndarray, lam: np.ndarray, mu_rows: np.ndarray,
-                    budget_s: float = 12.0) -> dict:
-    """Oracle port (oracle/oracle.c) on a bounded sample of C4, extrapolated:
-    the first S Householder steps (tred1, eigensolve.cpp:24-61) of K
-    concurrent minors scaled by the exact per-step cost model sum (l+1)^2,
-    plus the identity stage for K columns (identity.cpp:185-238)."""
+def _cores() -> int:
+    return os.cpu_count() or 1
+
+
+def _timed_reps(fn, budget_s: float, max_reps: int = 1000):
+    """Runs fn() until budget_s of wall time is used (at least once)."""
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        fn()
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= budget_s or reps >= max_reps:
+            return reps, dt
+
+
+# ----------------------------------------------------------------- CPU legs (oracle port)
+def cpu_c1(a: np.ndarray, g: np.ndarray) -> dict:
+    """Oracle port, full all_magnitudes n = 64 on all host threads."""
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    K = _cores()
+    n = a.shape[0]
+    reps, dt = _timed_reps(lambda: orc.all_magnitudes(a, threads=K), 2.0)
+    c = orc.all_magnitudes(a, threads=K)
+    return {"value": reps * n * n / dt, "unit": UNIT, "cores": K, "kind": "port",
+            "sample": f"full: oracle all_magnitudes n={n}, {reps} repetitions, {K} threads",
+            "parity": parity_record(g.reshape(n, n), c.reshape(n, n), "oracle port",
+                                    "full 64x64")}
+
+
+def cpu_c2(mats: np.ndarray, g: np.ndarray) -> dict:
+    """Oracle port, all 4096 matrices (one single-thread oracle call per
+    matrix, K threads) — the full config, a couple of seconds."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle.oracle import Oracle
     orc = Oracle()
-    K = os.cpu_count() or 1
+    K = _cores()
+    t = time.perf_counter()
+    with ThreadPoolExecutor(K) as ex:
+        outs = list(ex.map(lambda m: orc.all_magnitudes(m, threads=1), mats))
+    dt = time.perf_counter() - t
+    c = np.stack(outs).reshape(g.shape)
+    count, n = mats.shape[0], mats.shape[1]
+    return {"value": count * n * n / dt, "unit": UNIT, "cores": K, "kind": "port",
+            "sample": f"full: {count} x oracle all_magnitudes n={n} on {K} threads",
+            "parity": parity_record(g, c, "oracle port", f"all {count} matrices")}
+
+
+def cpu_c3(a: np.ndarray, lam_g: np.ndarray, mu_g: np.ndarray, g: np.ndarray) -> dict:
+    """Oracle port on a sample of C3: eig(A), K concurrent minor solves and
+    the identity for those K columns, extrapolated to n+1 solves and n
+    columns; parity of the GPU's spectra and rows on that sample."""
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    K = _cores()
+    n = a.shape[0]
+    js = [int(j) for j in np.linspace(0, n - 1, K).round()]
+    t = time.perf_counter()
+    lam = orc.eigenvalues(a)
+    t_eig = time.perf_counter() - t
+    t = time.perf_counter()
+    mu = orc.minor_spectra(a, js, threads=K)
+    t_batch = time.perf_counter() - t
+    t = time.perf_counter()
+    rows = orc.identity_rows(lam, mu, threads=K)
+    t_id = time.perf_counter() - t
+    total = t_eig + math.ceil(n / K) * t_batch + (n / K) * t_id
+    par = parity_record(g[js], rows, "oracle port", f"{K} rows j={js[0]}..{js[-1]}")
+    par["max_abs_lambda"] = float(np.max(np.abs(lam_g - lam)))
+    par["max_abs_mu"] = float(np.max(np.abs(mu_g[js] - mu)))
+    return {"value": n * n / total, "unit": UNIT, "cores": K, "kind": "port",
+            "sample": (f"oracle port: eig(A) + {K} concurrent minor solves + identity for "
+                       f"those {K} columns ({t_eig + t_batch + t_id:.1f} s), extrapolated "
+                       f"to n+1 solves and n columns"),
+            "extrapolated_seconds": total, "parity": par}
+
+
+def cpu_c4(n: int, a: np.ndarray, lam: np.ndarray, mu_rows: np.ndarray,
+           budget_s: float = 12.0) -> dict:
+    """Oracle port on a bounded sample of C4, extrapolated: the first S
+    Householder steps (tred1, eigensolve.cpp:24-61) of K concurrent minors
+    scaled by the exact per-step cost model sum (l+1)^2, plus the identity
+    stage for K columns (identity.cpp:185-238)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    K = _cores()
     m = n - 1
     minors = [orc.minor(a, j) for j in range(K)]
 
@@ -219,60 +322,102 @@ def cpu_baseline_c4(n: int, a: np.ndarray, lam: np.ndarray, mu_rows: np.ndarray,
             "extrapolated_seconds": total}
 
 
+def cpu_c5(lam: np.ndarray, mu_rows: np.ndarray, g_rows: np.ndarray, j0: int,
+           budget_s: float = 10.0) -> dict:
+    """Oracle port, identity only (cached spectra, evaluate() per component)
+    on a bounded sample of components over K threads, extrapolated to n^2;
+    each sampled component is compared with the GPU's bit for bit."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    K = _cores()
+    n = lam.shape[0]
+    rows = mu_rows.shape[0]
+    rng = np.random.default_rng(0)
+
+    def comps(count, seed):
+        r = np.random.default_rng(seed)
+        return list(zip(r.integers(0, rows, count), r.integers(0, n, count)))
+
+    def work(batch):
+        return [orc.evaluate(lam, mu_rows[r], int(i))[0] for r, i in batch]
+
+    t = time.perf_counter()
+    work(comps(4, 1))
+    per = max((time.perf_counter() - t) / 4, 1e-6)
+    m = max(4, int(budget_s / per))
+    batches = [comps(m, 100 + k) for k in range(K)]
+    t = time.perf_counter()
+    with ThreadPoolExecutor(K) as ex:
+        vals = list(ex.map(work, batches))
+    dt = time.perf_counter() - t
+    got = np.array([g_rows[r, i] for b in batches for r, i in b])
+    want = np.array([v for vs in vals for v in vs])
+    del rng
+    return {"value": K * m / dt, "unit": UNIT, "cores": K, "kind": "port",
+            "sample": (f"oracle port evaluate() on {K} x {m} random components of rows "
+                       f"j={j0}..{j0 + rows - 1} (cached spectra), rate x n^2"),
+            "parity": parity_record(got, want, "oracle port", f"{K * m} components",
+                                    rel=1e-10, abs_=0.0)}
+
+
+# ----------------------------------------------------------------- reference arm
 def reference_arm(args, cfg_desc: dict) -> dict:
-    """--impl reference: the unmodified reference (oracle/_ref) on this host."""
-    from oracle.oracle import Reference
-    ref = Reference()
-    K = os.cpu_count() or 1
+    """--impl reference: the unmodified reference (oracle/_ref) on this
+    host's cores.  Inputs come from oracle/_ref (random_symmetric), the
+    oracle (C3 / C5 generators) and the committed reference goldens, so no
+    product library is loaded.  Each timed step is one real, bounded sample
+    of the workload; `value` = components that sample produced / its time."""
+    K = _cores()
     wl = args.config
-    if wl in ("C4", "C3"):
+    line = _reference_config(wl, args.steps, args.warmup, K)
+    line.update({"metric": METRIC, "n_gpus": args.gpus, "steps": args.steps,
+                 "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                 "config": cfg_desc, "impl": "reference"})
+    if not args.no_subconfigs and args.gpus == 1 and wl == "C4":
+        line["configs"] = {}
+        for c in ("C1", "C2", "C3", "C5"):
+            sub = _reference_config(c, SUB_STEPS[c] if c != "C5" else 1, 1, K)
+            sub["config"] = config_desc(c, 1)
+            line["configs"][c] = sub
+    return line
+
+
+def _reference_config(wl: str, steps: int, warmup: int, K: int) -> dict:
+    from oracle.oracle import Oracle, Reference
+    ref = Reference()
+    warm = ref.random_symmetric(1, 64)
+    for _ in range(warmup):                   # cheap, untimed (no JIT on the CPU side)
+        ref.all_magnitudes(warm, workers=K)
+    times, units = [], 0
+    if wl in ("C3", "C4"):
         n = 4096 if wl == "C4" else 1024
-        a = goe_matrix(n) if wl == "C4" else c3_matrix(n)
-        if wl == "C3":
-            # full reference pipeline
-            for _ in range(args.warmup):
-                ref.all_magnitudes(goe_matrix(64))
-            times = []
-            for _ in range(args.steps):
-                t = time.perf_counter()
-                ref.all_magnitudes(a, workers=K)
-                times.append(time.perf_counter() - t)
-            tmean = statistics.mean(times)
-            value = n * n / tmean
-            sample = f"full all_magnitudes n={n} on {K} workers"
+        if wl == "C4":
+            a = ref.random_symmetric(42, n) * math.sqrt(2.0 / n)
+            lam = np.load(os.path.join(GOLDEN, "reference_c4.npz"))["lam"]
         else:
-            lam = np.linalg.eigvalsh(a)  # untimed input prep for the identity sample
-            for _ in range(args.warmup):  # bounded warm-up: small full pipeline
-                ref.all_magnitudes(goe_matrix(64))
-            times = []
-            js = list(range(K))
-            for s in range(args.steps):
-                jj = [(j + s * K) % n for j in js]
-                t = time.perf_counter()
-                mu = ref.minor_spectra(a, jj, workers=K)
-                t_solve = time.perf_counter() - t
-                t = time.perf_counter()
-                ref.identity_rows(lam, mu, workers=K)
-                t_id = time.perf_counter() - t
-                times.append(math.ceil((n + 1) / K) * t_solve + (n / K) * t_id)
-            tmean = statistics.mean(times)
-            value = n * n / tmean
-            sample = (f"per step: {K} concurrent reference minor solves "
-                      f"(eigenvalues(minor_matrix(j)), ThreadPool of {K}) + reference "
-                      f"identity for those {K} columns; extrapolated to n+1 solves and "
-                      f"n columns (eig(A) counted at minor cost; warm-up steps run "
-                      f"all_magnitudes at n=64)")
+            a = Oracle().c3_matrix(n, 3)
+            lam = np.load(os.path.join(GOLDEN, "reference_c3.npz"))["lam"]
+        for s in range(steps):
+            js = [(j + s * K) % n for j in range(K)]
+            t = time.perf_counter()
+            mu = ref.minor_spectra(a, js, workers=K)
+            ref.identity_rows(lam, mu, workers=K)
+            times.append(time.perf_counter() - t)
+            units += K * n
+        sample = (f"per step: {K} concurrent reference minor solves (eigenvalues("
+                  f"minor_matrix(j)) on the reference ThreadPool) + the reference "
+                  f"identity for those {K} columns = {K}x{n} components; lambda(A) is "
+                  f"the reference's own (committed golden), its one solve (1/{n + 1} of "
+                  f"the solves) is not timed; warm-up: all_magnitudes n=64")
     elif wl in ("C1", "C2"):
         n = 64 if wl == "C1" else 32
         count = 1 if wl == "C1" else 4096
-        from oracle.oracle import Oracle
-        orc = Oracle()
-        mats = [orc.random_symmetric(1 if wl == "C1" else b, n) for b in range(count)]
+        mats = [ref.random_symmetric(1 if wl == "C1" else b, n) for b in range(count)]
         from concurrent.futures import ThreadPoolExecutor
-        for _ in range(args.warmup):
-            ref.all_magnitudes(mats[0], workers=1)
-        times = []
-        for _ in range(args.steps):
+        for _ in range(steps):
             t = time.perf_counter()
             if count == 1:
                 ref.all_magnitudes(mats[0], workers=K)
@@ -280,31 +425,36 @@ def reference_arm(args, cfg_desc: dict) -> dict:
                 with ThreadPoolExecutor(K) as ex:
                     list(ex.map(lambda m_: ref.all_magnitudes(m_, workers=1), mats))
             times.append(time.perf_counter() - t)
-        tmean = statistics.mean(times)
-        value = count * n * n / tmean
-        sample = f"full: {count} x all_magnitudes n={n}"
-    else:  # C5: identity only, sampled columns
+            units += count * n * n
+        sample = (f"full: {count} x reference all_magnitudes n={n}"
+                  + (f" ({K} workers)" if count == 1 else
+                     f" (1-worker engines on {K} threads)"))
+    else:  # C5: identity only, sampled components
         n = 32768
-        from oracle.oracle import Oracle
         orc = Oracle()
-        lam = orc.c5_lambda(5, n)
-        times = []
-        for s in range(args.steps):
+        lam = orc.c5_lambda(C5_SEED, n)
+        from concurrent.futures import ThreadPoolExecutor
+        per_thread = 8000
+        for s in range(steps):
             rows = list(range(s * K, (s + 1) * K))
-            mu = orc.c5_mu_rows(5, lam, rows)
+            mu = orc.c5_mu_rows(C5_SEED, lam, rows)
+
+            def work(r):
+                rng = np.random.default_rng(1000 + r)
+                for i in rng.integers(0, n, per_thread):
+                    ref.component_magnitude_cached(lam, mu[r], int(i), rows[r])
             t = time.perf_counter()
-            ref.identity_rows(lam, mu, workers=K)
-            times.append((time.perf_counter() - t) * n / K)
-        tmean = statistics.mean(times)
-        value = n * n / tmean
-        sample = f"reference identity for {K} columns per step, x n/{K}"
-    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmean * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": cfg_desc,
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": K,
-                             "kind": "reference", "sample": sample},
+            with ThreadPoolExecutor(K) as ex:
+                list(ex.map(work, range(K)))
+            times.append(time.perf_counter() - t)
+            units += K * per_thread
+        sample = (f"per step: {K} threads x {per_thread} reference component_magnitude "
+                  f"calls with cached spectra (1-worker engines, SURVEY §3.4)")
+    t_all = sum(times)
+    value = units / t_all
+    return {"value": value, "unit": UNIT, "ms_per_step": t_all / len(times) * 1e3,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": K, "kind": "reference",
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -324,57 +474,55 @@ def config_desc(wl: str, world: int) -> dict:
     }[wl]
     d = dict(d)
     d["parallelism"] = f"j-shard x{world}"
-    d["l2"] = "inputs/working set larger than L2 (126 MB) for C4/C5; C1-C3 re-run from HBM"
+    d["l2"] = ("C4/C5: working set > L2 (126 MB); C1-C3: inputs re-read from HBM each "
+               "step, no L2 flush")
     return d
 
 
-def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
+def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
+               cpu: bool) -> dict | None:
     import torch
 
-    from paper_2002_04989_b200 import IdentityConfig, IdentityEngine
-    from paper_2002_04989_b200.shard import gather_rows, shard_range
-    torch.cuda.set_device(dist.local)
-    eng = IdentityEngine(IdentityConfig(), device=dist.local)
-    dev = eng.device
-    stream = torch.cuda.ExternalStream(dev.stream(), device=f"cuda:{dist.local}")
-    wl = args.config
-    world, rank = dist.world, dist.rank
-    n = cfg_desc["n"]
-
-    # ---- inputs in HBM
-    lam_host = mu_host = None
     from paper_2002_04989_b200 import random_symmetric
     from paper_2002_04989_b200.engine import c5_lambda
+    from paper_2002_04989_b200.shard import gather_rows, shard_range
+    dev = eng.device
+    stream = torch.cuda.ExternalStream(dev.stream(), device=f"cuda:{dist.local}")
+    world, rank = dist.world, dist.rank
+    cfg_desc = config_desc(wl, world)
+    n = cfg_desc["n"]
+    cuda = f"cuda:{dist.local}"
+    state = {}
+
+    # ---- inputs in HBM
     if wl in ("C1", "C3", "C4"):
         a_host = {"C1": lambda: random_symmetric(1, 64),
                   "C3": lambda: c3_matrix(1024), "C4": lambda: goe_matrix(4096)}[wl]()
-        a_dev = torch.from_numpy(a_host).to(f"cuda:{dist.local}")
+        a_dev = torch.from_numpy(a_host).to(cuda)
         j0, j1 = shard_range(n, world, rank)
         rows = j1 - j0
-        out_dev = torch.empty((rows, n), dtype=torch.float64, device=a_dev.device)
-        lam_dev = torch.empty(n, dtype=torch.float64, device=a_dev.device)
-        mu_dev = torch.empty((max(rows, 1), n - 1), dtype=torch.float64, device=a_dev.device)
-        full = None
+        out_dev = torch.empty((rows, n), dtype=torch.float64, device=cuda)
+        lam_dev = torch.empty(n, dtype=torch.float64, device=cuda)
+        mu_dev = torch.empty((max(rows, 1), n - 1), dtype=torch.float64, device=cuda)
         units = n * n
 
         def step():
-            nonlocal full
             eng.all_magnitudes_device(a_dev.data_ptr(), n, j0, j1, out_dev.data_ptr(),
                                       lam_dev.data_ptr(), mu_dev.data_ptr())
             if world > 1:
                 if dist.backend == "nccl":
                     with torch.cuda.stream(stream):
-                        full = gather_rows(out_dev, n, world, dist.pg)
+                        state["full"] = gather_rows(out_dev, n, world, dist.pg)
                 else:  # host collective (gloo): the rows travel through the CPU
                     stream.synchronize()
-                    full = gather_rows(out_dev.cpu(), n, world, dist.pg)
+                    state["full"] = gather_rows(out_dev.cpu(), n, world, dist.pg)
         flops = f_tri(n, rows) + f_id(n, rows)
     elif wl == "C2":
         count = 4096
         b0, b1 = shard_range(count, world, rank)
         a_host = np.stack([random_symmetric(b, 32) for b in range(b0, b1)])
-        a_dev = torch.from_numpy(a_host).to(f"cuda:{dist.local}")
-        out_dev = torch.empty((b1 - b0, 32 * 32), dtype=torch.float64, device=a_dev.device)
+        a_dev = torch.from_numpy(a_host).to(cuda)
+        out_dev = torch.empty((b1 - b0, 32 * 32), dtype=torch.float64, device=cuda)
         units = count * 32 * 32
 
         def step():
@@ -382,13 +530,13 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
         rows = n
         flops = (b1 - b0) * (f_tri(32, 32) + f_id(32, 32))
     else:  # C5
-        lam_host = c5_lambda(5, n)
-        lam_dev = torch.from_numpy(lam_host).to(f"cuda:{dist.local}")
+        lam_host = c5_lambda(C5_SEED, n)
+        lam_dev = torch.from_numpy(lam_host).to(cuda)
         j0, j1 = shard_range(n, world, rank)
         rows = j1 - j0
-        mu_dev = torch.empty((rows, n - 1), dtype=torch.float64, device=lam_dev.device)
-        eng.c5_mu_device(5, lam_dev.data_ptr(), n, j0, j1, mu_dev.data_ptr())
-        out_dev = torch.empty((rows, n), dtype=torch.float64, device=lam_dev.device)
+        mu_dev = torch.empty((rows, n - 1), dtype=torch.float64, device=cuda)
+        eng.c5_mu_device(C5_SEED, lam_dev.data_ptr(), n, j0, j1, mu_dev.data_ptr())
+        out_dev = torch.empty((rows, n), dtype=torch.float64, device=cuda)
         units = n * n
 
         def step():
@@ -397,11 +545,12 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
         flops = f_id(n, rows)
 
     # ---- warm-up, then K timed steps (device clock on the library stream)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     eng.sync()
-    dev.set_profiling(True)
-    stage1_ms = []
+    large = wl in ("C3", "C4")
+    dev.set_profiling(large)
+    stage_runs = []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(dist.local)
@@ -410,11 +559,10 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
     launches0 = dev.launch_count()
     clocks.start()
     ev0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
-        if wl in ("C3", "C4"):
-            stream.synchronize()
-            stage1_ms.append(dev.stage_times()["stage1"])
+        if large:   # stage events are on the library stream; read per call
+            stage_runs.append(dev.stage_times())
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
@@ -424,22 +572,23 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
     eng.sync()
     dev.set_profiling(False)
     t_total = dist.max(ev0.elapsed_time(ev1) / 1e3)
-    value = units * args.steps / t_total
-    ms_step = t_total / args.steps * 1e3
+    value = units * steps / t_total
+    ms_step = t_total / steps * 1e3
 
     # ---- end to end through the public API with host buffers
     e2e = None
-    e2e_steps = max(1, args.steps // 2)
+    e2e_steps = max(1, min(steps // 4, 5)) if wl == "C4" else max(1, min(steps // 2, 5))
+    res = None
     if wl in ("C1", "C3", "C4"):
         if world == 1:
             t = time.perf_counter()
             for _ in range(e2e_steps):
                 res = eng.all_magnitudes(a_host)   # H2D A, pipeline, D2H |v|^2
             te = time.perf_counter() - t
-            float(res[0])
-            e2e = {"value": units * e2e_steps / te, "unit": UNIT,
+            e2e = {"value": units * e2e_steps / te, "unit": UNIT, "steps": e2e_steps,
                    "h2d_bytes_per_step": a_host.nbytes,
-                   "d2h_bytes_per_step": res.nbytes + n * 8}
+                   "d2h_bytes_per_step": res.nbytes,
+                   "api": "IdentityEngine.all_magnitudes (host numpy in, host numpy out)"}
         else:
             pin = torch.from_numpy(a_host).pin_memory()
             out_pin = torch.empty((n, n), dtype=torch.float64).pin_memory()
@@ -453,22 +602,24 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
                     a_dev.copy_(pin, non_blocking=True)
                 step()
                 with torch.cuda.stream(stream):
-                    out_pin.copy_(full, non_blocking=True)
+                    out_pin.copy_(state["full"], non_blocking=True)
             if dist.backend != "nccl":
                 torch.cuda.synchronize()
             e1.record(stream)
             e1.synchronize()
             te = dist.max(e0.elapsed_time(e1) / 1e3)
-            e2e = {"value": units * e2e_steps / te, "unit": UNIT,
-                   "h2d_bytes_per_step": a_host.nbytes, "d2h_bytes_per_step": n * n * 8}
+            e2e = {"value": units * e2e_steps / te, "unit": UNIT, "steps": e2e_steps,
+                   "h2d_bytes_per_step": a_host.nbytes, "d2h_bytes_per_step": n * n * 8,
+                   "api": "pinned H2D + all_magnitudes_device + NCCL all-gather + D2H"}
     elif wl == "C2":
         if world == 1:
             t = time.perf_counter()
             for _ in range(e2e_steps):
                 res = eng.all_magnitudes_batched(a_host)
             te = time.perf_counter() - t
-            e2e = {"value": units * e2e_steps / te, "unit": UNIT,
-                   "h2d_bytes_per_step": a_host.nbytes, "d2h_bytes_per_step": res.nbytes}
+            e2e = {"value": units * e2e_steps / te, "unit": UNIT, "steps": e2e_steps,
+                   "h2d_bytes_per_step": a_host.nbytes, "d2h_bytes_per_step": res.nbytes,
+                   "api": "IdentityEngine.all_magnitudes_batched"}
     else:
         if world == 1:
             mu_host = mu_dev.cpu().numpy()
@@ -476,58 +627,112 @@ def our_arm(args, dist: Dist, cfg_desc: dict) -> dict | None:
             for _ in range(e2e_steps):
                 res = eng.identity(lam_host, mu_host)
             te = time.perf_counter() - t
-            e2e = {"value": units * e2e_steps / te, "unit": UNIT,
+            e2e = {"value": units * e2e_steps / te, "unit": UNIT, "steps": e2e_steps,
                    "h2d_bytes_per_step": lam_host.nbytes + mu_host.nbytes,
-                   "d2h_bytes_per_step": res.nbytes}
+                   "d2h_bytes_per_step": res.nbytes,
+                   "api": "IdentityEngine.identity (cached spectra, host buffers)"}
 
-    # ---- roofline of the dominant kernel
-    if wl in ("C3", "C4"):
-        t1 = statistics.mean(stage1_ms) / 1e3
-        achieved = f_tri(n, rows) / t1 / 1e12
-        # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
-        # --set full capture of 296 solves (profiles/
-        # r01h_band_4096_wide_raw_summary.csv: 2.053 TB read + 1.231 TB
-        # written), scaled to this launch's solve count
-        traffic = (2.052512e12 + 1.230878e12) / 296 * (rows + 1) if n == 4096 else None
-        roof = {"bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
-                "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": traffic,
-                "traffic_note": ("ncu dram__bytes_read+write per solve x solves; "
-                                 "HBM rate = traffic / launch time"),
-                "hbm_GBps": (traffic / t1 / 1e9) if traffic else None,
-                "ceiling_note": ("cuBLAS DGEMM on the stage-1 update shapes reaches 18.9 "
-                                 "(n=32 SYMM) / 20.3 (k=64 SYR2K) TFLOP/s on this B200 "
-                                 "(profiles/r01_cublas_dgemm_ceilings.txt)"),
-                "peak_source": P_FP64_SOURCE,
-                "algorithmic": "F_tri = (4/3)[n^3 + rows (n-1)^3] flops per launch",
-                "launch_ms": t1 * 1e3, "share_of_step": t1 * 1e3 / ms_step}
-    else:
-        achieved = flops / (ms_step / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": "whole step", "achieved": achieved,
-                "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": None,
-                "peak_source": P_FP64_SOURCE,
-                "algorithmic": "F_tri + F_id (C2) or F_id = 4 n^2 (n-1) (C5) per step"}
-
+    # ---- roofline of the dominant kernel (+ the other stages)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": cfg_desc,
             "matrices_per_sec": (1e3 / ms_step) * (4096 if wl == "C2" else 1),
             "fp64_frac_whole_step": flops * world / (ms_step / 1e3) / 1e12 / (
                 P_FP64_MEASURED_TFLOPS * world),
-            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "roofline": roof}
-    if wl in ("C3", "C4"):
-        line["stage_ms"] = dev.stage_times()
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+    if large:
+        st = {k: statistics.mean(r[k] for r in stage_runs) for k in stage_runs[0]}
+        t1 = st["stage1"] / 1e3
+        achieved = f_tri(n, rows) / t1 / 1e12
+        # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
+        # --set full capture (profiles/r01h_band_4096_wide_raw_summary.csv:
+        # 2.053 TB read + 1.231 TB written over 296 solves), scaled to this
+        # launch's solve count
+        traffic = (2.052512e12 + 1.230878e12) / 296 * (rows + 1) if n == 4096 else None
+        line["roofline"] = {
+            "bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
+            "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": traffic,
+            "traffic_note": "ncu dram__bytes_read+write per solve x solves",
+            "hbm_GBps": (traffic / t1 / 1e9) if traffic else None,
+            "peak_source": P_FP64_SOURCE,
+            "algorithmic": "F_tri = (4/3)[n^3 + rows (n-1)^3] flops per launch",
+            "launch_ms": t1 * 1e3, "share_of_step": t1 * 1e3 / ms_step}
+        line["stage_ms"] = st
+        line["stages"] = {
+            "stage2_bulge_chase": {"ms": st["stage2"], "TFLOP/s": f_chase(n, rows) /
+                                   (st["stage2"] / 1e3) / 1e12,
+                                   "algorithmic": "6 b m^2 per solve, b = 32"},
+            "identity": {"ms": st["identity"], "TFLOP/s": f_id(n, rows) /
+                         (st["identity"] / 1e3) / 1e12 if st["identity"] > 0 else None,
+                         "algorithmic": "F_id = 4 n (n-1) per row"},
+            "lambda_A_side_stream_ms": st["lambda_A"],
+            "bisect_minors_ms": st["bisect_minors"]}
+    else:
+        achieved = flops / (ms_step / 1e3) / 1e12
+        line["roofline"] = {
+            "bound": "tensor",
+            "kernel": "identity_kernel (whole step)" if wl == "C5" else "whole step",
+            "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": None,
+            "peak_source": P_FP64_SOURCE,
+            "algorithmic": ("F_id = 4 n^2 (n-1) per step (2 DP ops per triple are issued "
+                            "after hoisting the denominator: FP64-pipe share ~ frac/2)"
+                            if wl == "C5" else "F_tri + F_id per step")}
 
-    # ---- CPU baseline (rank 0, N = 1 only)
-    if world == 1 and not args.no_cpu_baseline and wl == "C4":
-        lam_h = lam_dev.cpu().numpy()
-        mu_h = mu_dev[: os.cpu_count() or 1].cpu().numpy()
-        line["cpu_baseline"] = cpu_baseline_c4(n, a_host, lam_h, mu_h)
-    elif world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = None
+    # ---- parity (golden fixtures) and CPU baseline (rank 0, N = 1 only)
+    if world == 1:
+        g = out_dev.cpu().numpy()
+        if wl == "C1":
+            gold = np.load(os.path.join(GOLDEN, "reference_golden.npz"))
+            line["parity"] = parity_record(g, gold["s1_n64_all64"], "reference golden",
+                                           "full 64x64 (reference_golden.npz s1_n64)")
+        elif wl in ("C3", "C4"):
+            gold = np.load(os.path.join(GOLDEN, f"reference_{wl.lower()}.npz"))
+            js = gold["js"]
+            lam_g = lam_dev.cpu().numpy()
+            mu_g = mu_dev.cpu().numpy()
+            par = parity_record(g[js], gold["rows"], "reference golden (oracle/_ref)",
+                                f"{len(js)} rows j in {list(map(int, js))}")
+            par["max_abs_lambda"] = float(np.max(np.abs(lam_g - gold["lam"])))
+            par["max_abs_mu_sampled"] = float(np.max(np.abs(mu_g[js] - gold["mu"])))
+            line["parity"] = par
+        if cpu and not args.no_cpu_baseline:
+            if wl == "C1":
+                line["cpu_baseline"] = cpu_c1(a_host, g)
+            elif wl == "C2":
+                line["cpu_baseline"] = cpu_c2(a_host, g)
+                line["parity"] = line["cpu_baseline"].pop("parity")
+            elif wl == "C3":
+                line["cpu_baseline"] = cpu_c3(a_host, lam_dev.cpu().numpy(),
+                                              mu_dev.cpu().numpy(), g)
+                line["cpu_baseline"]["parity_vs_oracle"] = line["cpu_baseline"].pop("parity")
+            elif wl == "C4":
+                mu_h = mu_dev[: _cores()].cpu().numpy()
+                line["cpu_baseline"] = cpu_c4(n, a_host, lam_dev.cpu().numpy(), mu_h)
+            else:
+                line["cpu_baseline"] = cpu_c5(lam_host, mu_dev[:64].cpu().numpy(), g[:64], 0)
+                line["parity"] = line["cpu_baseline"].pop("parity")
     return line if rank == 0 else None
+
+
+def our_arm(args, dist: Dist) -> dict | None:
+    import torch
+
+    from paper_2002_04989_b200 import IdentityConfig, IdentityEngine
+    torch.cuda.set_device(dist.local)
+    eng = IdentityEngine(IdentityConfig(), device=dist.local)
+    line = our_config(args, dist, eng, args.config, args.steps, args.warmup, cpu=True)
+    if line is not None and dist.world == 1 and args.config == "C4" and not args.no_subconfigs:
+        line["configs"] = {}
+        for c in ("C1", "C2", "C3", "C5"):
+            sub = our_config(args, dist, eng, c, SUB_STEPS[c], 2, cpu=True)
+            for k in ("metric", "unit", "n_gpus", "higher_is_better", "scaling",
+                      "vs_baseline", "dtype", "data"):
+                sub.pop(k, None)
+            line["configs"][c] = sub
+    return line
 
 
 def main():
@@ -538,19 +743,21 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-subconfigs", action="store_true",
+                    help="only the headline config (the N>1 runs never add them)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo lets several ranks share one GPU (flow testing only)")
     args = ap.parse_args()
     dist = Dist()
-    cfg = config_desc(args.config, dist.world)
     if args.impl == "reference":
         if dist.rank != 0:
             return 0
-        print(json.dumps(reference_arm(args, cfg)), flush=True)
+        print(json.dumps(reference_arm(args, config_desc(args.config, dist.world))),
+              flush=True)
         return 0
     dist.init(args.dist_backend)
     try:
-        line = our_arm(args, dist, cfg)
+        line = our_arm(args, dist)
     finally:
         dist.close()
     if line is not None:

@@ -18,7 +18,19 @@
  *    No exception ever crosses this boundary; the host layers re-throw the
  *    matching eigenid::Error subclass (proj/include/eigenid/errors.hpp).
  *  - *_device entry points take device pointers and a cudaStream_t (passed as
- *    void*), enqueue work, and report errors at the next eigenid_gpu_sync().
+ *    void*), enqueue work, and report errors at the next eigenid_gpu_sync()
+ *    (or the next host-pointer call, which also reads the status).  The
+ *    status is sticky: the FIRST error of the enqueued calls is reported,
+ *    and every stage of a later enqueued call stops early once it is set.
+ *  - Input matrices are checked for non-finite entries on the device
+ *    (EIGENID_E_NONFINITE_ENTRY, err->index = entry, before any solve), as
+ *    SymmetricMatrix::build does (matrix.cpp:17-18).
+ *  - A degenerate lambda(A) (EIGENID_E_DEGENERATE) stops the minor solves
+ *    early: lambda(A) is solved first, beside the minors, and the minors'
+ *    work queues stop pulling once the degeneracy check fails
+ *    (identity.cpp:299-300 throws before any minor solve).
+ *  - A bisection that exhausts its iteration budget, or a non-finite
+ *    tridiagonal, is EIGENID_E_CONVERGENCE (eigensolve.cpp:90-93).
  *  - There is no CPU fallback: a missing device is EIGENID_E_DEVICE.
  */
 #ifndef EIGENID_B200_H
@@ -45,6 +57,11 @@ enum eigenid_status {
   EIGENID_E_INDEX = 7,            /* IndexOutOfRange       errors.hpp:26-29 */
   EIGENID_E_SIGN_RECOVERY = 8,    /* SignRecoveryFailure   errors.hpp:79-82 */
   EIGENID_E_DIMENSION = 9,        /* DimensionMismatch     errors.hpp:46-49 */
+  EIGENID_E_NONFINITE_ENTRY = 10, /* NonFiniteEntry        errors.hpp:21-24,
+                                     raised by build(), matrix.cpp:17-18 */
+  EIGENID_E_ASYMMETRIC = 11,      /* AsymmetricInput       errors.hpp:16-19
+                                     (host mirrors only: the ABI reads the
+                                     lower triangle) */
   EIGENID_E_DEVICE = 20,          /* new: CUDA failure / no device          */
   EIGENID_E_ALLOC = 21            /* new: device allocation failed          */
 };
@@ -201,6 +218,12 @@ void eigenid_random_symmetric(uint64_t seed, size_t n, int uniform,
 /* The raw SeededDraws stream (matrix_io.cpp:44-65): `count` Gaussian
  * (kind 0) or uniform(-1,1) (kind 1) draws. */
 void eigenid_seeded_draws(uint64_t seed, size_t count, int kind, double* out);
+
+/* C3 input: Q diag(linspace(-1,1)) Q^T with Q the sign-fixed
+ * Householder QR factor of an n x n seeded Gaussian matrix, symmetrised as
+ * build(kSymmetrize) does.  Deterministic plain loops (no BLAS): the same
+ * bytes on every host. */
+void eigenid_c3_matrix(uint64_t seed, size_t n, double* out);
 
 /* Number of kernels this context has launched (instrumentation for the
  * bench's gpu_launches field). */

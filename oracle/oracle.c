@@ -705,3 +705,76 @@ int orc_recover_signs(const double* a, size_t n, size_t i, const double* mags,
   }
   return ORC_OK;
 }
+
+/* C3 input: A = Q diag(lambda) Q^T with Q from the Householder
+ * QR of an n x n matrix G of SeededDraws::gaussian draws (matrix_io.cpp:53-65,
+ * row-major), each column of Q sign-fixed by diag(R); lambda_k = -1 + 2k/(n-1);
+ * then build(kSymmetrize) (matrix.cpp:30-35).  Plain loops in a fixed order
+ * (no BLAS), so the product library's eigenid_c3_matrix reproduces it bit for
+ * bit and the reference arm can build the same bytes without the product. */
+void orc_c3_matrix(uint64_t seed, size_t n, double* out) {
+  double* g = (double*)malloc(sizeof(double) * n * n);
+  double* w = (double*)malloc(sizeof(double) * n * n);   /* W = G^T: row k = column k */
+  double* p = (double*)malloc(sizeof(double) * n * n);   /* P = Q^T */
+  double* beta = (double*)malloc(sizeof(double) * n);
+  double* rdiag = (double*)malloc(sizeof(double) * n);
+  orc_gaussian_stream(seed, n * n, g);
+  for (size_t r = 0; r < n; ++r)
+    for (size_t c = 0; c < n; ++c) w[c * n + r] = g[r * n + c];
+  for (size_t k = 0; k < n; ++k) {
+    double* x = w + k * n;
+    double ss = 0.0;
+    for (size_t t = k; t < n; ++t) ss += x[t] * x[t];
+    const double nrm = sqrt(ss);
+    const double alpha = x[k] >= 0.0 ? -nrm : nrm;
+    rdiag[k] = alpha;
+    if (nrm == 0.0) { beta[k] = 0.0; continue; }
+    x[k] -= alpha;                       /* v = x - alpha e_k, stored in place */
+    double vv = 0.0;
+    for (size_t t = k; t < n; ++t) vv += x[t] * x[t];
+    beta[k] = 2.0 / vv;
+    for (size_t j = k + 1; j < n; ++j) {
+      double* y = w + j * n;
+      double d = 0.0;
+      for (size_t t = k; t < n; ++t) d += x[t] * y[t];
+      const double s = beta[k] * d;
+      for (size_t t = k; t < n; ++t) y[t] -= s * x[t];
+    }
+  }
+  /* Q = H_0 ... H_{n-1}: backward accumulation on P = Q^T from the right */
+  for (size_t t = 0; t < n * n; ++t) p[t] = 0.0;
+  for (size_t t = 0; t < n; ++t) p[t * n + t] = 1.0;
+  for (size_t k = n; k-- > 0;) {
+    const double* v = w + k * n;
+    if (beta[k] == 0.0) continue;
+    for (size_t r = k; r < n; ++r) {
+      double* pr = p + r * n;
+      double d = 0.0;
+      for (size_t t = k; t < n; ++t) d += pr[t] * v[t];
+      const double s = beta[k] * d;
+      for (size_t t = k; t < n; ++t) pr[t] -= s * v[t];
+    }
+  }
+  /* column k of Q (row k of P) times sign(R_kk) */
+  for (size_t k = 0; k < n; ++k)
+    if (rdiag[k] < 0.0)
+      for (size_t t = 0; t < n; ++t) p[k * n + t] = -p[k * n + t];
+  /* A = sum_k lambda_k q_k q_k^T, rank-1 updates in k order */
+  for (size_t t = 0; t < n * n; ++t) out[t] = 0.0;
+  for (size_t k = 0; k < n; ++k) {
+    const double lk = -1.0 + 2.0 * (double)k / (double)(n - 1);
+    const double* q = p + k * n;
+    for (size_t r = 0; r < n; ++r) {
+      const double s = lk * q[r];
+      double* ar = out + r * n;
+      for (size_t c = 0; c < n; ++c) ar[c] += s * q[c];
+    }
+  }
+  for (size_t r = 0; r < n; ++r)
+    for (size_t c = r + 1; c < n; ++c) {
+      const double m = 0.5 * (out[r * n + c] + out[c * n + r]);
+      out[r * n + c] = m;
+      out[c * n + r] = m;
+    }
+  free(g); free(w); free(p); free(beta); free(rdiag);
+}

@@ -47,6 +47,8 @@ typedef struct {
 /* ---- seeded inputs: src/matrix_io.cpp:39-71, :171-181; src/matrix.cpp ---- */
 void orc_random_symmetric(uint64_t seed, size_t n, int uniform, double* out);
 void orc_gaussian_stream(uint64_t seed, size_t count, double* out);
+/* C3 input, SURVEY §8 d3 (bit-identical to eigenid_c3_matrix) */
+void orc_c3_matrix(uint64_t seed, size_t n, double* out);
 uint64_t orc_splitmix64(uint64_t x); /* src/bench.cpp:78-83 */
 void orc_minor(const double* a, size_t n, size_t j, double* out); /* matrix.cpp:51-68 */
 

@@ -51,6 +51,7 @@ class Oracle:
         L = self.lib = C.CDLL(path)
         L.orc_random_symmetric.argtypes = [C.c_uint64, C.c_size_t, C.c_int, _dp]
         L.orc_gaussian_stream.argtypes = [C.c_uint64, C.c_size_t, _dp]
+        L.orc_c3_matrix.argtypes = [C.c_uint64, C.c_size_t, _dp]
         L.orc_splitmix64.argtypes = [C.c_uint64]
         L.orc_splitmix64.restype = C.c_uint64
         L.orc_minor.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
@@ -81,6 +82,12 @@ class Oracle:
     def random_symmetric(self, seed: int, n: int, uniform: bool = False):
         out = np.empty((n, n), np.float64)
         self.lib.orc_random_symmetric(seed, n, int(uniform), _p(out))
+        return out
+
+    def c3_matrix(self, n: int = 1024, seed: int = 3):
+        """SURVEY §8 d3 input (bit-identical to the product's eigenid_c3_matrix)."""
+        out = np.empty((n, n), np.float64)
+        self.lib.orc_c3_matrix(seed, n, _p(out))
         return out
 
     def gaussian_stream(self, seed: int, count: int):

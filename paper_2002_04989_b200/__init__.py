@@ -11,11 +11,12 @@ from .errors import (AsymmetricInput, ConfigError, ConvergenceFailure,  # noqa: 
                      IndexOutOfRange, InternalInconsistency, MatrixTooSmall,
                      NonFiniteEntry, NonFiniteIntermediate, SignRecoveryFailure)
 from .engine import (Device, IdentityConfig, IdentityEngine,  # noqa: F401
-                     SymmetricMatrix, eigenvalues, random_symmetric, recover_signs)
+                     SymmetricMatrix, c3_matrix, eigenvalues, random_symmetric,
+                     recover_signs)
 
 __all__ = [
     "IdentityEngine", "IdentityConfig", "SymmetricMatrix", "eigenvalues", "Device",
-    "random_symmetric", "recover_signs",
+    "random_symmetric", "recover_signs", "c3_matrix",
     "Error", "MatrixTooSmall", "DegenerateEigenvalue", "ConvergenceFailure",
     "NonFiniteIntermediate", "InternalInconsistency", "ConfigError",
     "IndexOutOfRange", "DeviceError", "AsymmetricInput", "NonFiniteEntry",

@@ -84,6 +84,7 @@ SIGNATURES = {
     "eigenid_gpu_launch_count": (C.c_uint64, [C.c_void_p]),
     "eigenid_random_symmetric": (None, [C.c_uint64, C.c_size_t, C.c_int, _dp]),
     "eigenid_seeded_draws": (None, [C.c_uint64, C.c_size_t, C.c_int, _dp]),
+    "eigenid_c3_matrix": (None, [C.c_uint64, C.c_size_t, _dp]),
     "eigenid_gpu_set_profiling": (None, [C.c_void_p, C.c_int]),
     "eigenid_gpu_stage_times": (C.c_int, [C.c_void_p, _dp, C.c_int]),
 }

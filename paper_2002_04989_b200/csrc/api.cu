@@ -42,14 +42,22 @@ __global__ void init_status_kernel(DevStatus* st) {
   st[1].aux = -1;
 }
 
-// Solve list of one chunk: local t <-> global g = g0 + t; g = 0 is A itself
-// (-1), g >= 1 is minor j0 + g - 1.
+// Solve list of one chunk of minors: js[t] = j0 + g0 + t.
 __global__ void solve_list_kernel(int* js, int j0, int g0, int count) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count;
-       t += gridDim.x * blockDim.x) {
-    const int g = g0 + t;
-    js[t] = g == 0 ? -1 : j0 + g - 1;
-  }
+       t += gridDim.x * blockDim.x)
+    js[t] = j0 + g0 + t;
+}
+
+// SymmetricMatrix::build rejects non-finite entries before anything is
+// solved (matrix.cpp:17-18 -> NonFiniteEntry); the raw C-ABI takes plain
+// pointers, so the check runs on the device as the first kernel of a call
+// (every later stage aborts on the sticky status).  aux = matrix index.
+__global__ void nonfinite_kernel(const double* __restrict__ a, long long per,
+                                 long long total, DevStatus* st) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(a[t])) set_status(st, EIGENID_E_NONFINITE_ENTRY, t % per, 0.0, t / per);
 }
 
 }  // namespace eigenid_b200
@@ -87,11 +95,17 @@ struct DevBuf {
 struct eigenid_gpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // lambda(A)'s solve, beside the minors
+  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_a0 = nullptr;
   std::mutex mu;
   DevStatus* dstatus = nullptr;
   DevStatus* hstatus = nullptr;  // pinned
+  // A *_device call enqueued work whose status nobody has read yet: the
+  // status stays sticky (not re-initialised) until eigenid_gpu_sync or the
+  // next host-pointer call reads it.
+  bool pending = false;
   DevBuf bA, bOut, bLam, bMu, bDen, bRcp, bFlags, bFlagCount, bWs, bBand, bD,
-      bE2, bAe, bJs, bTmpOut, bTmpMu, bCounter;
+      bE2, bAe, bJs, bTmpOut, bTmpMu, bCounter, bBandA, bDeA, bJsA, bScale;
   std::atomic<size_t> solves{0};
   std::atomic<uint64_t> launches{0};
   bool profiling = false;
@@ -153,6 +167,7 @@ int finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
            "status copy");
   EID_CUDA(cudaStreamSynchronize(c->stream), "stream sync");
   EID_CUDA(cudaGetLastError(), "kernel launch");
+  c->pending = false;
   const DevStatus s = c->hstatus[0];
   if (degenerate) *degenerate = false;
   if (s.code == 0) return EIGENID_OK;
@@ -176,7 +191,13 @@ int finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
                     "ordering is inconsistent (i=%lld)", s.index);
       break;
     case EIGENID_E_CONVERGENCE:
-      std::snprintf(buf, sizeof buf, "eigenvalue solve did not converge");
+      std::snprintf(buf, sizeof buf,
+                    "eigenvalue solve did not converge (eigenvalue %lld of solve %lld)",
+                    s.index, s.aux);
+      break;
+    case EIGENID_E_NONFINITE_ENTRY:
+      std::snprintf(buf, sizeof buf, "matrix entry is not finite (entry %lld, matrix %lld)",
+                    s.index, s.aux);
       break;
     default:
       std::snprintf(buf, sizeof buf, "device error code %d", s.code);
@@ -187,8 +208,23 @@ int finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
 
 int begin(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
   EID_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  if (c->pending) return EIGENID_OK;  // an unread device-call status is sticky
   init_status_kernel<<<1, 1, 0, c->stream>>>(c->dstatus);
   EID_CUDA(cudaGetLastError(), "init_status");
+  c->launches += 1;
+  return EIGENID_OK;
+}
+
+int check_finite(eigenid_gpu_ctx* c, const double* dA, size_t per, size_t count,
+                 eigenid_gpu_err* err) {
+  const long long total = (long long)(per * count);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  long long blocks = (total + 255) / 256;
+  if (blocks > 8LL * sms) blocks = 8LL * sms;
+  nonfinite_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(dA, (long long)per, total,
+                                                           c->dstatus);
+  EID_CUDA(cudaGetLastError(), "nonfinite check");
   c->launches += 1;
   return EIGENID_OK;
 }
@@ -199,7 +235,7 @@ int begin(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
 // Same-box A/B: the wide stage-1 layout wins at n = 4096, the
 // narrow one at n = 1024.
 constexpr int kStage1WideMinN = 3072;
-constexpr int kStages = 5;  // stage1, stage2, bisect_A, bisect_minors, identity
+constexpr int kStages = 5;  // stage1, stage2, lambda_A (side), bisect_minors, identity
 struct StageTimer {
   bool on = false, print = false;
   cudaStream_t st = nullptr;
@@ -207,6 +243,7 @@ struct StageTimer {
   int slot[4 * kStages + 1];
   int count = 0;
   double* sink = nullptr;  // ctx->stage_ms
+  double side_ms = 0.0;     // A's pipeline on the side stream (slot 2)
   StageTimer(cudaStream_t s, bool enabled, double* out) : st(s), sink(out) {
     const char* e = std::getenv("EIGENID_PROFILE");
     print = e && e[0] == '1';
@@ -221,10 +258,12 @@ struct StageTimer {
   }
   ~StageTimer() {
     if (!on) return;
-    static const char* names[kStages] = {"stage1", "stage2", "bisect_A",
+    if (print) std::fprintf(stderr, "[eigenid] %-14s %10.3f ms (side stream)\n", "lambda(A)", side_ms);
+    static const char* names[kStages] = {"stage1", "stage2", "lambda_A",
                                          "bisect_minors", "identity"};
     cudaEventSynchronize(ev[count - 1]);
     for (int t = 0; t < kStages; ++t) sink[t] = 0.0;
+    sink[2] = side_ms;
     for (int t = 1; t < count; ++t) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[t - 1], ev[t]);
@@ -236,20 +275,29 @@ struct StageTimer {
 };
 
 // Large-n pipeline for minor rows [j0, j1) of a device matrix.
+//
+// lambda(A) is solved on the context's side stream while the minors run on
+// the main stream: A's stage 1 takes the SM the minors' persistent stage-1
+// grid leaves free, then its chase, bisection and the degeneracy check
+// (identity.cpp:299-300) run there too, and only then does that SM join the
+// minors' work queue (the "helper" launch).  A degenerate lambda(A) sets the
+// sticky status, so every stage's work queue stops pulling minors about one
+// A-solve after the call started instead of after all n minor solves — the
+// reference throws before it solves any minor.
 int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
               const eigenid_gpu_config* cfg, double* dout, double* dlam,
               double* dmu, bool identity, eigenid_gpu_err* err) {
-  cudaStream_t st = c->stream;
-  const int rows = j1 - j0;
-  const int nsolves = 1 + rows;  // global solve g: 0 = A, g >= 1 = minor j0+g-1
+  cudaStream_t st = c->stream, sa = c->side;
+  const int rows = j1 - j0;  // minors; A is solved separately
   const int kB = stage1_bandwidth();
   const int ldab = stage1_band_ld();
   const int ldw = (n + 7) & ~7;
   const long long ws_stride = stage1_ws_doubles(n, ldw);
   const long long band_stride = (long long)n * ldab;
-  // Memory plan: stage-1 workspace slots and the number of solves whose band
+  (void)kB;
+  // Memory plan: stage-1 workspace slots and the number of minors whose band
   // and tridiagonal are resident at once, sized to the free device memory
-  // (large n is processed in chunks of solves).
+  // (large n is processed in chunks of minors).
   size_t free_b = 0, total_b = 0;
   EID_CUDA(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   const double held = (double)(c->bWs.bytes + c->bBand.bytes + c->bD.bytes +
@@ -273,63 +321,111 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
     if (std::strcmp(lay, "wide") == 0) wide = true;
     if (std::strcmp(lay, "narrow") == 0) wide = false;
   }
-  const int max_slots = sms * (wide ? wide::stage1_ctas_per_sm() : narrow::stage1_ctas_per_sm());
-  int slots = nsolves < max_slots ? nsolves : max_slots;
+  const int cps = wide ? wide::stage1_ctas_per_sm() : narrow::stage1_ctas_per_sm();
+  auto launch1 = [&](const Stage1Args& a, int grid, cudaStream_t s, bool reset) {
+    return wide ? wide::launch_stage1(a, grid, s, reset)
+                : narrow::launch_stage1(a, grid, s, reset);
+  };
+  const int max_slots = sms * cps;
+  // one SM's worth of slots is reserved for A's pipeline (then the helper)
+  int slots = rows + cps < max_slots ? rows + cps : max_slots;
   while (slots > 1 && slots * ws_bytes > 0.7 * budget) slots = (slots + 1) / 2;
-  long long chunk = (long long)((budget - slots * ws_bytes) / solve_bytes);
-  if (chunk > nsolves) chunk = nsolves;
+  long long chunk = (long long)((budget - slots * ws_bytes - solve_bytes) / solve_bytes);
+  if (chunk > rows) chunk = rows;
   if (chunk < slots) chunk = slots;
   if (chunk < 1) chunk = 1;
+  const bool side_ok = slots > cps;   // else A runs first, alone
+  const int slot_a = side_ok ? slots - cps : 0;
   int launches = 0;
   EID_CUDA(c->bJs.ensure(sizeof(int) * (size_t)chunk), "alloc js");
+  EID_CUDA(c->bJsA.ensure(sizeof(int)), "alloc jsA");
   EID_CUDA(c->bWs.ensure(sizeof(double) * (size_t)slots * ws_stride), "alloc ws");
   EID_CUDA(c->bBand.ensure(sizeof(double) * (size_t)chunk * band_stride), "alloc band");
+  EID_CUDA(c->bBandA.ensure(sizeof(double) * (size_t)band_stride), "alloc bandA");
   EID_CUDA(c->bD.ensure(sizeof(double) * (size_t)chunk * n), "alloc d");
   EID_CUDA(c->bE2.ensure(sizeof(double) * (size_t)chunk * n), "alloc e2");
   EID_CUDA(c->bAe.ensure(sizeof(double) * (size_t)chunk * n), "alloc ae");
-  EID_CUDA(c->bCounter.ensure(sizeof(int) * 4), "alloc counter");
+  EID_CUDA(c->bDeA.ensure(sizeof(double) * 3 * (size_t)n), "alloc deA");
+  EID_CUDA(c->bCounter.ensure(sizeof(int) * 8), "alloc counter");
   int* djs = c->bJs.as<int>();
+  int* djsA = c->bJsA.as<int>();
+  int* ctr = c->bCounter.as<int>();  // [0] chase, [1] stage 1, [2] A stage 1, [3] A chase
+  double* dA_d = c->bDeA.as<double>();
 
   StageTimer timer(st, c->profiling, c->stage_ms);
-  for (long long g0 = 0; g0 < nsolves; g0 += chunk) {
-    const int cnt = (int)((nsolves - g0) < chunk ? (nsolves - g0) : chunk);
-    solve_list_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(djs, j0, (int)g0, cnt);
+  // first chunk's solve list and queue, before A's pipeline forks off
+  const int cnt0 = (int)(rows < chunk ? rows : chunk);
+  EID_CUDA(cudaMemsetAsync(djsA, 0xff, sizeof(int), st), "jsA");  // -1 = A itself
+  if (cnt0 > 0) {
+    solve_list_kernel<<<(cnt0 + 255) / 256, 256, 0, st>>>(djs, j0, 0, cnt0);
     ++launches;
-    Stage1Args s1{dA, n, djs, cnt, c->bWs.as<double>(), ws_stride, ldw,
-                  c->bBand.as<double>(), band_stride, c->bCounter.as<int>() + 1};
-    const int grid1 = cnt < slots ? cnt : slots;
-    EID_CUDA(wide ? wide::launch_stage1(s1, grid1, st) : narrow::launch_stage1(s1, grid1, st),
-             "stage1");
+    EID_CUDA(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st), "counter");
+  }
+  EID_CUDA(c->bScale.ensure(sizeof(double) * 4), "alloc scale");
+  double* dscale = c->bScale.as<double>();
+  EID_CUDA(launch_input_scale(dA, (long long)n * n, dscale, st, &launches), "input scale");
+  // EIGENID_BISECT_MAX_IT lowers the per-eigenvalue iteration budget (tests
+  // drive the ConvergenceFailure path with it)
+  int max_it = 300;
+  if (const char* mi = std::getenv("EIGENID_BISECT_MAX_IT")) max_it = std::atoi(mi);
+  EID_CUDA(cudaEventRecord(c->ev_start, st), "event");
+  EID_CUDA(cudaStreamWaitEvent(sa, c->ev_start, 0), "event wait");
+  // ---- side stream: lambda(A), the degeneracy check, then the helper
+  EID_CUDA(cudaEventRecord(c->ev_a0, sa), "event");
+  Stage1Args s1a{dA, n, djsA, 1, c->bWs.as<double>(), ws_stride, ldw,
+                 c->bBandA.as<double>(), band_stride, ctr + 2, c->dstatus, slot_a,
+                 dscale};
+  EID_CUDA(launch1(s1a, 1, sa, true), "stage1 A");
+  Stage2Args s2a{c->bBandA.as<double>(), band_stride, djsA, 1, n, dA_d, dA_d + n,
+                 dA_d + 2 * n, n, ctr + 3, c->dstatus, c->device};
+  EID_CUDA(launch_stage2(s2a, sa), "stage2 A");
+  BisectArgs ba{dA_d, dA_d + n, dA_d + 2 * n, n, djsA, 1, 0, n, nullptr, dlam, n,
+                (n + 255) / 256, c->dstatus, dscale, max_it};
+  EID_CUDA(launch_bisect(ba, 1, n, sa, &launches), "bisect A");
+  launches += 2;
+  if (identity)
+    EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol, c->dstatus, sa, &launches),
+             "degeneracy");
+  Stage1Args s1{dA, n, djs, cnt0, c->bWs.as<double>(), ws_stride, ldw,
+                c->bBand.as<double>(), band_stride, ctr + 1, c->dstatus, 0, dscale};
+  const int grid_main = side_ok ? (cnt0 < slot_a ? cnt0 : slot_a) : (cnt0 < slots ? cnt0 : slots);
+  if (side_ok && cnt0 > grid_main) {
+    Stage1Args h = s1;
+    h.slot0 = slot_a;
+    const int hg = cnt0 - grid_main < cps ? cnt0 - grid_main : cps;
+    EID_CUDA(launch1(h, hg, sa, false), "stage1 helper");
+    ++launches;
+  }
+  EID_CUDA(cudaEventRecord(c->ev_a, sa), "event");
+
+  // ---- main stream: the minors, chunk by chunk
+  if (!side_ok) EID_CUDA(cudaStreamWaitEvent(st, c->ev_a, 0), "event wait");
+  for (long long g0 = 0; g0 < rows; g0 += chunk) {
+    const int cnt = (int)((rows - g0) < chunk ? (rows - g0) : chunk);
+    if (g0 == 0) {
+      EID_CUDA(launch1(s1, grid_main, st, false), "stage1");
+      EID_CUDA(cudaStreamWaitEvent(st, c->ev_a, 0), "event wait");
+    } else {
+      solve_list_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(djs, j0, (int)g0, cnt);
+      ++launches;
+      s1.nsolves = cnt;
+      EID_CUDA(launch1(s1, cnt < slots ? cnt : slots, st, true), "stage1");
+    }
     ++launches;
     timer.mark(0);
     Stage2Args s2{c->bBand.as<double>(), band_stride, djs, cnt, n,
                   c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
-                  n, c->bCounter.as<int>()};
+                  n, ctr, c->dstatus, c->device};
     EID_CUDA(launch_stage2(s2, st), "stage2");
     ++launches;
     timer.mark(1);
-    int first = 0;
-    if (g0 == 0) {
-      // lambda(A): Gershgorin brackets, split across CTAs
-      BisectArgs ba{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
-                    n, djs, cnt, 0, n, nullptr, dlam, n, (n + 255) / 256};
-      EID_CUDA(launch_bisect(ba, 1, n, st, &launches), "bisect A");
-      timer.mark(2);
-      if (identity)
-        EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol, c->dstatus, st,
-                                   &launches),
-                 "degeneracy");
-      first = 1;
-    }
-    if (cnt > first) {
-      // minors of this chunk -> mu rows (g0 + first - 1) ..
-      BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
-                    n, djs, cnt, first, n, dlam,
-                    dmu + (size_t)(g0 + first - 1) * (n - 1), n - 1, 1};
-      EID_CUDA(launch_bisect(bm, cnt - first, n - 1, st, &launches), "bisect minors");
-      timer.mark(3);
-    }
+    BisectArgs bm{c->bD.as<double>(), c->bE2.as<double>(), c->bAe.as<double>(),
+                  n, djs, cnt, 0, n, dlam, dmu + (size_t)g0 * (n - 1), n - 1, 1,
+                  c->dstatus, dscale, max_it};
+    EID_CUDA(launch_bisect(bm, cnt, n - 1, st, &launches), "bisect minors");
+    timer.mark(3);
   }
+  if (rows == 0) EID_CUDA(cudaStreamWaitEvent(st, c->ev_a, 0), "event wait");
   if (identity && rows > 0) {
     const int batch = batch_of(cfg, n);
     const int nb = identity_nb(n, batch);
@@ -345,6 +441,12 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
                              cfg->log_domain, st, &launches),
              "identity");
     timer.mark(4);
+  }
+  if (timer.on) {  // A's pipeline on the side stream (stage slot 2)
+    float ms = 0.f;
+    cudaEventSynchronize(c->ev_a);
+    cudaEventElapsedTime(&ms, c->ev_a0, c->ev_a);
+    timer.side_ms = ms;
   }
   c->launches += launches;
   return EIGENID_OK;
@@ -465,6 +567,71 @@ void eigenid_random_symmetric(uint64_t seed, size_t n, int uniform, double* e) {
       }
 }
 
+// C3 input: Householder QR of the seeded Gaussian G
+// (row-major draws), Q sign-fixed by diag(R), A = Q diag(linspace(-1,1)) Q^T,
+// build(kSymmetrize).  Plain loops in a fixed order, no BLAS, so every host
+// produces the same bytes (a LAPACK QR differs across CPU kernels).
+void eigenid_c3_matrix(uint64_t seed, size_t n, double* out) {
+  std::vector<double> g(n * n), w(n * n), p(n * n, 0.0), beta(n), rdiag(n);
+  eigenid_seeded_draws(seed, n * n, 0, g.data());
+  for (size_t r = 0; r < n; ++r)
+    for (size_t c = 0; c < n; ++c) w[c * n + r] = g[r * n + c];
+  for (size_t k = 0; k < n; ++k) {  // W = G^T; row k holds column k
+    double* x = w.data() + k * n;
+    double ss = 0.0;
+    for (size_t t = k; t < n; ++t) ss += x[t] * x[t];
+    const double nrm = std::sqrt(ss);
+    const double alpha = x[k] >= 0.0 ? -nrm : nrm;
+    rdiag[k] = alpha;
+    if (nrm == 0.0) {
+      beta[k] = 0.0;
+      continue;
+    }
+    x[k] -= alpha;  // Householder vector v = x - alpha e_k, in place
+    double vv = 0.0;
+    for (size_t t = k; t < n; ++t) vv += x[t] * x[t];
+    beta[k] = 2.0 / vv;
+    for (size_t j = k + 1; j < n; ++j) {
+      double* y = w.data() + j * n;
+      double d = 0.0;
+      for (size_t t = k; t < n; ++t) d += x[t] * y[t];
+      const double sc = beta[k] * d;
+      for (size_t t = k; t < n; ++t) y[t] -= sc * x[t];
+    }
+  }
+  for (size_t t = 0; t < n; ++t) p[t * n + t] = 1.0;  // P = Q^T, backward accumulation
+  for (size_t k = n; k-- > 0;) {
+    if (beta[k] == 0.0) continue;
+    const double* v = w.data() + k * n;
+    for (size_t r = k; r < n; ++r) {
+      double* pr = p.data() + r * n;
+      double d = 0.0;
+      for (size_t t = k; t < n; ++t) d += pr[t] * v[t];
+      const double sc = beta[k] * d;
+      for (size_t t = k; t < n; ++t) pr[t] -= sc * v[t];
+    }
+  }
+  for (size_t k = 0; k < n; ++k)
+    if (rdiag[k] < 0.0)
+      for (size_t t = 0; t < n; ++t) p[k * n + t] = -p[k * n + t];
+  for (size_t t = 0; t < n * n; ++t) out[t] = 0.0;
+  for (size_t k = 0; k < n; ++k) {  // A = sum_k lambda_k q_k q_k^T
+    const double lk = -1.0 + 2.0 * (double)k / (double)(n - 1);
+    const double* q = p.data() + k * n;
+    for (size_t r = 0; r < n; ++r) {
+      const double sc = lk * q[r];
+      double* ar = out + r * n;
+      for (size_t c = 0; c < n; ++c) ar[c] += sc * q[c];
+    }
+  }
+  for (size_t r = 0; r < n; ++r)
+    for (size_t c = r + 1; c < n; ++c) {
+      const double m = 0.5 * (out[r * n + c] + out[c * n + r]);
+      out[r * n + c] = m;
+      out[c * n + r] = m;
+    }
+}
+
 void eigenid_seeded_draws(uint64_t seed, size_t count, int kind, double* out) {
   SeededDraws d(seed);
   for (size_t t = 0; t < count; ++t) out[t] = kind ? d.uniform_open() : d.gaussian();
@@ -500,6 +667,10 @@ int eigenid_gpu_create(eigenid_gpu_ctx** out, int device, eigenid_gpu_err* err) 
   if ((e = cudaSetDevice(device)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) !=
           cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreate(&c->ev_a)) != cudaSuccess ||
+      (e = cudaEventCreate(&c->ev_a0)) != cudaSuccess ||
       (e = cudaMalloc(&c->dstatus, 2 * sizeof(DevStatus))) != cudaSuccess ||
       (e = cudaMallocHost(&c->hstatus, 2 * sizeof(DevStatus))) != cudaSuccess) {
     delete c;
@@ -516,10 +687,14 @@ int eigenid_gpu_destroy(eigenid_gpu_ctx* c) {
   for (DevBuf* b : {&c->bA, &c->bOut, &c->bLam, &c->bMu, &c->bDen, &c->bRcp,
                     &c->bFlags, &c->bFlagCount, &c->bWs, &c->bBand, &c->bD,
                     &c->bE2, &c->bAe, &c->bJs, &c->bTmpOut, &c->bTmpMu,
-                    &c->bCounter})
+                    &c->bCounter, &c->bBandA, &c->bDeA, &c->bJsA, &c->bScale})
     b->release();
   cudaFree(c->dstatus);
   cudaFreeHost(c->hstatus);
+  cudaEventDestroy(c->ev_start);
+  cudaEventDestroy(c->ev_a);
+  cudaEventDestroy(c->ev_a0);
+  cudaStreamDestroy(c->side);
   cudaStreamDestroy(c->stream);
   delete c;
   return EIGENID_OK;
@@ -565,6 +740,7 @@ int eigenid_gpu_eigenvalues(eigenid_gpu_ctx* c, const double* a, size_t n,
   EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
                            cudaMemcpyHostToDevice, c->stream),
            "H2D A");
+  if ((st = check_finite(c, c->bA.as<double>(), n * n, 1, err))) return st;
   eigenid_gpu_config cfg{64, 0.0, 0};
   st = run_large(c, c->bA.as<double>(), (int)n, 0, 0, &cfg, nullptr,
                  c->bLam.as<double>(), nullptr, false, err);
@@ -592,6 +768,7 @@ int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
   EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * nn,
                            cudaMemcpyHostToDevice, c->stream),
            "H2D A");
+  if ((st = check_finite(c, c->bA.as<double>(), nn, 1, err))) return st;
   st = run_all(c, c->bA.as<double>(), (int)n, 0, (int)n, cfg,
                c->bOut.as<double>(), c->bLam.as<double>(), c->bMu.as<double>(),
                err);
@@ -611,7 +788,10 @@ int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
   st = finish(c, err, &degenerate);
   // identity.cpp:299-306: lambda(A) is solved, then the degeneracy check
   // throws before the n minor solves.
-  c->solves += (st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1;
+  // NonFiniteEntry: build() throws before any solve (matrix.cpp:17-18)
+  c->solves += st == EIGENID_E_NONFINITE_ENTRY
+                   ? 0
+                   : ((st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1);
   return st;
 }
 
@@ -631,6 +811,7 @@ int eigenid_gpu_all_magnitudes_batched(eigenid_gpu_ctx* c, const double* a,
   EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * tot,
                            cudaMemcpyHostToDevice, c->stream),
            "H2D A");
+  if ((st = check_finite(c, c->bA.as<double>(), n * n, count, err))) return st;
   if (n <= (size_t)kSmallMax) {
     EID_CUDA(launch_small_all(c->bA.as<double>(), count, (int)n,
                               batch_of(cfg, (int)n), cfg->degeneracy_tol,
@@ -674,6 +855,7 @@ int eigenid_gpu_minor_spectra(eigenid_gpu_ctx* c, const double* a, size_t n,
   EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
                            cudaMemcpyHostToDevice, c->stream),
            "H2D A");
+  if ((st = check_finite(c, c->bA.as<double>(), n * n, 1, err))) return st;
   eigenid_gpu_config cfg{64, 0.0, 0};
   st = run_large(c, c->bA.as<double>(), (int)n, (int)j0, (int)j1, &cfg, nullptr,
                  c->bLam.as<double>(), c->bMu.as<double>(), false, err);
@@ -731,9 +913,15 @@ int eigenid_gpu_identity_device(eigenid_gpu_ctx* c, const double* d_lambda,
   if (n < 2) return check_n(n, err);
   int st = check_cfg(cfg, err);
   if (st) return st;
+  if (j0 > j1 || j1 > n) {
+    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, "row range out of bounds");
+    return EIGENID_E_INDEX;
+  }
   std::lock_guard<std::mutex> g(c->mu);
   if ((st = begin(c, err))) return st;
-  return identity_impl(c, d_lambda, d_mu, n, j0, j1, cfg, d_out, err);
+  st = identity_impl(c, d_lambda, d_mu, n, j0, j1, cfg, d_out, err);
+  c->pending = true;
+  return st;
 }
 
 }  // extern "C"
@@ -783,6 +971,8 @@ int eigenid_gpu_all_magnitudes_device(eigenid_gpu_ctx* c, const double* d_a,
   }
   std::lock_guard<std::mutex> g(c->mu);
   if ((st = begin(c, err))) return st;
+  c->pending = true;
+  if ((st = check_finite(c, d_a, n * n, 1, err))) return st;
   st = run_all(c, d_a, (int)n, (int)j0, (int)j1, cfg, d_out, d_lambda, d_mu, err);
   if (st == EIGENID_OK) c->solves += 1 + (j1 - j0);
   return st;
@@ -804,6 +994,8 @@ int eigenid_gpu_all_magnitudes_batched_device(eigenid_gpu_ctx* c,
   }
   std::lock_guard<std::mutex> g(c->mu);
   if ((st = begin(c, err))) return st;
+  c->pending = true;
+  if ((st = check_finite(c, d_a, n * n, count, err))) return st;
   EID_CUDA(launch_small_all(d_a, count, (int)n, batch_of(cfg, (int)n),
                             cfg->degeneracy_tol, cfg->log_domain, d_out,
                             nullptr, nullptr, c->dstatus, c->stream),
@@ -832,6 +1024,7 @@ int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
   EID_CUDA(c->bOut.ensure(sizeof(double) * n), "alloc out");
   EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
                            cudaMemcpyHostToDevice, c->stream), "H2D A");
+  if ((st = check_finite(c, c->bA.as<double>(), n * n, 1, err))) return st;
   eigenid_gpu_config scfg{64, 0.0, 0};
   st = run_large(c, c->bA.as<double>(), (int)n, 0, (int)n, &scfg, nullptr,
                  c->bLam.as<double>(), c->bMu.as<double>(), false, err);
@@ -967,6 +1160,7 @@ int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* c, const double* a,
     EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
     EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
                              cudaMemcpyHostToDevice, c->stream), "H2D A");
+    if ((st = check_finite(c, c->bA.as<double>(), n * n, 1, err))) return st;
     eigenid_gpu_config scfg{64, 0.0, 0};
     st = run_large(c, c->bA.as<double>(), (int)n, (int)j, (int)j + 1, &scfg,
                    nullptr, c->bLam.as<double>(), c->bMu.as<double>(), false,

@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
   const int n = args.n, ldw = args.ldw;
   // slot workspace: the minor (n x ldw), then V and X (= W2) for two panels
   // and VT, n x kB each (stage1_ws_doubles)
-  double* W = args.ws + blockIdx.x * args.ws_stride;
+  double* W = args.ws + (long long)(args.slot0 + blockIdx.x) * args.ws_stride;
   double* const Vg[2] = {W + (long long)n * ldw, W + (long long)n * ldw + (long long)n * kB};
   double* const Xg[2] = {W + (long long)n * ldw + 2LL * n * kB,
                          W + (long long)n * ldw + 3LL * n * kB};
@@ -1099,7 +1099,10 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
   // them running alone at the end of every wave.
   __shared__ int s_sidx;
   for (;;) {
-    if (tid == 0) s_sidx = atomicAdd(args.counter, 1);
+    // a failed call (non-finite input, degenerate lambda(A)) stops pulling
+    if (tid == 0)
+      s_sidx = *(volatile const int*)&args.status->code ? args.nsolves
+                                                        : atomicAdd(args.counter, 1);
     __syncthreads();
     const int sidx = s_sidx;
     __syncthreads();
@@ -1108,7 +1111,9 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
     const int m = j < 0 ? n : n - 1;
     double* band = args.band + sidx * args.band_stride;
     PHASE(1);
-    // materialise the lower triangle of the minor (r' = r + (r >= j))
+    // materialise the lower triangle of the minor (r' = r + (r >= j)),
+    // times the exact power-of-two input scale
+    const double in_sc = args.scale ? args.scale[0] : 1.0;
     for (int r = warp; r < m; r += kNT / 32) {
       const int rr = (j >= 0 && r >= j) ? r + 1 : r;
       const double* src = args.A + (long long)rr * n;
@@ -1118,7 +1123,7 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int cc = c0 + 32 * u;
-          v[u] = cc <= r ? src[(j >= 0 && cc >= j) ? cc + 1 : cc] : 0.0;
+          v[u] = cc <= r ? src[(j >= 0 && cc >= j) ? cc + 1 : cc] * in_sc : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u)
@@ -1243,13 +1248,16 @@ extern "C" void eigenid_debug_cta_span(unsigned long long* out) {
 size_t stage1_smem_bytes() { return sizeof(double) * (size_t)kStage1SmemDoubles; }
 int stage1_ctas_per_sm() { return kCtasPerSm; }
 
-cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st) {
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st,
+                          bool reset) {
   const size_t smem = stage1_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(
       band_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
+  if (reset) {
+    e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
   band_reduce_kernel<<<grid, kNT, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -37,18 +37,19 @@ __device__ double block_reduce_min(double v, double* red) {
 // One eigenvalue's bracketing / secant state machine (see bisect_kernel).
 struct BisectLane {
   int k = 0;
-  bool active = false, gersh = false;
+  bool active = false, gersh = false, failed = false;
+  int failed_k = -1;
   int stage = 0, it = 0, side = 0, clo = 0, chi = 0, elo = 0, ehi = 0;
   double lo = 0.0, hi = 0.0, plo = 0.0, phi = 0.0, w1 = 0.0, w2 = 0.0;
 
   __device__ __forceinline__ void start(const double* lam, double delta, double glo,
                                         double ghi, double sc, double glo_s,
-                                        double ghi_s) {
+                                        double ghi_s, double as) {
     stage = 0;
     if (lam) {
       gersh = false;
-      lo = fmax(lam[k] - delta, glo) * sc;
-      hi = fmin(lam[k + 1] + delta, ghi) * sc;
+      lo = fmax(lam[k] * as - delta, glo) * sc;
+      hi = fmin(lam[k + 1] * as + delta, ghi) * sc;
     } else {
       gersh = true;
       lo = glo_s;
@@ -60,13 +61,14 @@ struct BisectLane {
   __device__ __forceinline__ double next_x(double atol, double* out, double sc, int stride,
                                            int k1, const double* lam, double delta,
                                            double glo, double ghi, double glo_s,
-                                           double ghi_s) {
+                                           double ghi_s, double as, double us,
+                                           int max_it) {
     double x = 0.0;
     if (stage == 2) {
       bool fin = false;
       const double w = hi - lo;
       const double tol = fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)));
-      if (w <= tol || it >= 300) {
+      if (w <= tol || it >= max_it) {
         fin = true;
       } else {
         x = lo + 0.5 * w;
@@ -90,11 +92,18 @@ struct BisectLane {
 #ifdef EIGENID_BISECT_STATS
         atomicAdd(&g_bis_hist[it < 63 ? it : 63], 1ull);
 #endif
-        out[k] = (lo + 0.5 * (hi - lo)) / sc;
+        const double v = (lo + 0.5 * (hi - lo)) / sc * us;
+        // iteration budget exhausted or a non-finite tridiagonal: the
+        // reference's QL raises ConvergenceFailure (eigensolve.cpp:90-93)
+        if (((it >= max_it && w > tol) || !isfinite(v)) && !failed) {
+          failed = true;
+          failed_k = k;
+        }
+        out[k] = v;
         k += stride;
         active = k < k1;
         if (active) {
-          start(lam, delta, glo, ghi, sc, glo_s, ghi_s);
+          start(lam, delta, glo, ghi, sc, glo_s, ghi_s, as);
           x = lo;
         }
       }
@@ -158,6 +167,7 @@ __global__ void __launch_bounds__(kBisNT, kBisMinBlocks) bisect_kernel(BisectArg
   __shared__ int unsorted;
   const int solve = a.first_solve + blockIdx.x / a.split;
   const int part = blockIdx.x % a.split;
+  if (*(volatile const int*)&a.status->code) return;  // the call already failed
   const int m = a.js[solve] < 0 ? a.n : a.n - 1;
   double* sd = sm;
   double* se2 = sm + m;
@@ -201,14 +211,16 @@ __global__ void __launch_bounds__(kBisNT, kBisMinBlocks) bisect_kernel(BisectArg
   // counts at both ends; if either check fails the lane restarts on the
   // Gershgorin interval.
   const double glo_s = glo * sc, ghi_s = ghi * sc;
+  const double as = a.scale ? a.scale[0] : 1.0, us = a.scale ? a.scale[1] : 1.0;
   BisectLane ln;
   ln.k = k0 + threadIdx.x;
   ln.active = ln.k < k1;
-  if (ln.active) ln.start(a.lam, delta, glo, ghi, sc, glo_s, ghi_s);
+  if (ln.active) ln.start(a.lam, delta, glo, ghi, sc, glo_s, ghi_s, as);
   while (__any_sync(0xffffffffu, ln.active)) {
     double x = 0.0;
     if (ln.active)
-      x = ln.next_x(atol, out, sc, kBisNT, k1, a.lam, delta, glo, ghi, glo_s, ghi_s);
+      x = ln.next_x(atol, out, sc, kBisNT, k1, a.lam, delta, glo, ghi, glo_s, ghi_s, as,
+                    us, a.max_it);
     if (ln.active) {
       double px;
       int ex;
@@ -216,6 +228,7 @@ __global__ void __launch_bounds__(kBisNT, kBisMinBlocks) bisect_kernel(BisectArg
       ln.update(cx, px, ex, x, glo_s, ghi_s);
     }
   }
+  if (ln.failed) set_status(a.status, 3, ln.failed_k, 0.0, solve);
   if (a.split > 1) return;  // cross-CTA order is checked by sort_fix_kernel
   __syncthreads();
   if (threadIdx.x == 0) unsorted = 0;
@@ -255,6 +268,42 @@ __global__ void sort_fix_kernel(double* out, int m) {
       out[t + 1] = v;
     }
   }
+}
+
+// max|a| -> exact power-of-two scale (see kernels.cuh)
+__global__ void input_maxabs_kernel(const double* __restrict__ a, long long count,
+                                    unsigned long long* maxbits) {
+  double m = 0.0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count;
+       t += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(a[t]));
+  m = warp_max(m);
+  // non-negative doubles order like their bit patterns
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(m));
+}
+__global__ void input_scale_kernel(const unsigned long long* maxbits, double* scale) {
+  const double m = __longlong_as_double((long long)*maxbits);
+  double s = 1.0, u = 1.0;
+  if (m > 0x1p400 || (m > 0.0 && m < 0x1p-400)) {
+    const int e = ilogb(m);
+    s = scalbn(1.0, -e);
+    u = scalbn(1.0, e);
+  }
+  scale[0] = s;
+  scale[1] = u;
+}
+
+cudaError_t launch_input_scale(const double* dA, long long count, double* dscale,
+                               cudaStream_t st, int* launches) {
+  auto* bits = reinterpret_cast<unsigned long long*>(dscale + 2);
+  cudaError_t e = cudaMemsetAsync(bits, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  long long blocks = (count + 255) / 256;
+  if (blocks > 2048) blocks = 2048;
+  input_maxabs_kernel<<<(unsigned)blocks, 256, 0, st>>>(dA, count, bits);
+  input_scale_kernel<<<1, 1, 0, st>>>(bits, dscale);
+  *launches += 2;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,

@@ -277,7 +277,9 @@ bulge_chase_kernel(Stage2Args a) {
 
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_sidx = atomicAdd(a.counter, 1);
+    if (threadIdx.x == 0)
+      s_sidx = *(volatile const int*)&a.status->code ? a.nsolves
+                                                     : atomicAdd(a.counter, 1);
     if (threadIdx.x < kWarpsPerCta) prog[threadIdx.x] = -1;
     __syncthreads();
     const int sidx = s_sidx;
@@ -439,7 +441,7 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a.device);
   const int slots = sms * kBulgeCtasPerSm;
   const int grid = a.nsolves < slots ? a.nsolves : slots;
   bool long_sweeps = a.n >= kWarpsLongMinN;

@@ -99,7 +99,8 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
                 int n, int rows, int batch, int nb,
                 const double* __restrict__ den, const double* __restrict__ rcp,
                 double* __restrict__ out, unsigned long long* flag_count,
-                long long* flags, long long flag_cap) {
+                long long* flags, long long flag_cap, const DevStatus* status) {
+  if (*(volatile const int*)&status->code) return;  // the call already failed
   __shared__ double smu[2][kIdTJ * (kIdCH + 1)];
   __shared__ double sden[2][2 * kIdTI];  // den, rcp of the batch ending in a chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -124,21 +125,23 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
 
   const int total = n - 1;  // number of factor pairs
   const int nchunks = (total + kIdCH - 1) / kIdCH;
-  // With batch >= kIdCH at most one batch ends inside a chunk; its den/rcp
-  // rows for this CTA's 256 i are staged with the chunk (cp.async) instead of
-  // being loaded at the batch end.
+  // With batch >= kIdCH at most one full batch ends inside a chunk, plus the
+  // short final batch in the last chunk.  The den/rcp rows (this CTA's 256 i)
+  // of the LAST batch ending in a chunk are staged with the chunk (cp.async);
+  // any other batch ending there (only the one before a short final batch)
+  // reads den/rcp from global memory at its end.
   const bool staged_den = batch >= kIdCH;
+  // the last batch whose final pair lies in chunk c, or -1
+  auto chunk_bend = [&](int c) -> int {
+    const int s0 = c * kIdCH, s1 = min(s0 + kIdCH, total);
+    if (s1 == total) return (total - 1) / batch;
+    const int bend = s1 / batch - 1;
+    return (bend < 0 || (bend + 1) * batch - 1 < s0) ? -1 : bend;
+  };
   auto stage_den = [&](int c, int buf) {
     if (!staged_den) return;
-    const int s0 = c * kIdCH, s1 = min(s0 + kIdCH, total);
-    // the batch whose last pair lies in [s0, s1), if any
-    int bend;
-    if (s1 == total) {
-      bend = (total - 1) / batch;
-    } else {
-      bend = s1 / batch - 1;
-      if (bend < 0 || (bend + 1) * batch - 1 < s0) return;
-    }
+    const int bend = chunk_bend(c);
+    if (bend < 0) return;
     for (int t = threadIdx.x; t < kIdTI; t += blockDim.x) {
       const long long g = (long long)min(i0 + t, n - 1) * nb + bend;
       cp_async8(&sden[buf][t], den + g);
@@ -162,6 +165,7 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
     __syncthreads();
     const double* sm = smu[c & 1] + (warp * kIdPJ) * (kIdCH + 1);
     const int s0 = c * kIdCH, s1 = min(s0 + kIdCH, total);
+    const int cb = staged_den ? chunk_bend(c) : -1;
     int s = s0;
     while (s < s1) {
       const int stop = min(s1, batch_end);
@@ -179,7 +183,7 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
 #pragma unroll
         for (int q = 0; q < kIdQI; ++q) {
           double dq, rq;
-          if (staged_den) {
+          if (staged_den && b == cb) {
             dq = sden[c & 1][lane + 32 * q];
             rq = sden[c & 1][kIdTI + lane + 32 * q];
           } else {
@@ -212,6 +216,9 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
       if (isfinite(raw)) {
         orow[ii[q]] = clamp01(raw);
       } else {
+        // NaN marks the entry for the retry; past the flag buffer's capacity
+        // the retry finds it by scanning the output instead
+        orow[ii[q]] = __longlong_as_double(0x7ff8000000000000ll);
         const unsigned long long slot = atomicAdd(flag_count, 1ull);
         if ((long long)slot < flag_cap) flags[slot] = (long long)r * n + ii[q];
       }
@@ -221,31 +228,50 @@ identity_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
 
 // Log-domain retry for flagged components (identity.cpp:227-231), and the
 // whole stage when IdentityConfig::Evaluation::kLogDomain is selected.
+__device__ __forceinline__ void log_domain_fix_one(const double* __restrict__ lam,
+                                                   const double* __restrict__ mu,
+                                                   int n, long long idx,
+                                                   double* __restrict__ out,
+                                                   DevStatus* status) {
+  const int r = (int)(idx / n), i = (int)(idx % n);
+  double v;
+  const int rc = identity_log_domain(lam, mu + (long long)r * (n - 1), n, i, &v);
+  if (rc)
+    set_status(status, rc, i, 0.0, r);
+  else
+    out[idx] = clamp01(v);
+}
+
+// When more components were flagged than the buffer holds (e.g. a matrix
+// scaled by 1e6, where every batch product overflows), the whole output is
+// scanned for the NaN markers identity_kernel left instead.
 __global__ void log_domain_fix_kernel(const double* __restrict__ lam,
                                       const double* __restrict__ mu, int n,
+                                      int rows,
                                       const unsigned long long* flag_count,
-                                      const long long* flags,
+                                      const long long* flags, long long flag_cap,
                                       double* __restrict__ out,
                                       DevStatus* status) {
+  if (*(volatile const int*)&status->code) return;
   const unsigned long long cnt = *flag_count;
-  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x +
-                              threadIdx.x;
-       t < cnt; t += (unsigned long long)gridDim.x * blockDim.x) {
-    const long long idx = flags[t];
-    const int r = (int)(idx / n), i = (int)(idx % n);
-    double v;
-    const int rc = identity_log_domain(lam, mu + (long long)r * (n - 1), n, i, &v);
-    if (rc)
-      set_status(status, rc, i, 0.0, r);
-    else
-      out[idx] = clamp01(v);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long t0 =
+      blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  if (cnt > (unsigned long long)flag_cap) {
+    const unsigned long long total = (unsigned long long)rows * n;
+    for (unsigned long long t = t0; t < total; t += stride)
+      if (isnan(out[t])) log_domain_fix_one(lam, mu, n, (long long)t, out, status);
+    return;
   }
+  for (unsigned long long t = t0; t < cnt; t += stride)
+    log_domain_fix_one(lam, mu, n, flags[t], out, status);
 }
 
 __global__ void log_domain_all_kernel(const double* __restrict__ lam,
                                       const double* __restrict__ mu, int n,
                                       int rows, double* __restrict__ out,
                                       DevStatus* status) {
+  if (*(volatile const int*)&status->code) return;
   const long long total = (long long)rows * n;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
        t < total; t += (long long)gridDim.x * blockDim.x) {
@@ -406,9 +432,9 @@ cudaError_t launch_identity(const double* dlam, const double* dmu, int n,
   dim3 grid((n + kIdTI - 1) / kIdTI, (rows + kIdTJ - 1) / kIdTJ);
   identity_kernel<<<grid, 256, 0, st>>>(dlam, dmu, n, rows, batch, nb, dden,
                                         drcp, dout, dflag_count, dflags,
-                                        flag_cap);
-  log_domain_fix_kernel<<<148, 256, 0, st>>>(dlam, dmu, n, dflag_count, dflags,
-                                             dout, dstatus);
+                                        flag_cap, dstatus);
+  log_domain_fix_kernel<<<148 * 4, 256, 0, st>>>(dlam, dmu, n, rows, dflag_count,
+                                                 dflags, flag_cap, dout, dstatus);
   *launches += 3;
   return cudaGetLastError();
 }

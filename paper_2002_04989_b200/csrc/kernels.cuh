@@ -28,16 +28,21 @@ struct Stage1Args {
   int ldw;            // leading dimension of the slot matrix
   double* band;       // per-solve band, column-major [col][0..2kB]
   long long band_stride;
-  int* counter;       // work queue (zeroed before launch)
+  int* counter;       // work queue (zeroed before launch unless reset == 0)
+  const DevStatus* status;  // sticky call status: nonzero code = abort
+  int slot0;          // workspace slot of blockIdx.x == 0
+  const double* scale;  // [0]: exact power-of-two input scale (nullable = 1)
 };
 // Two compiled layouts of the same kernel (band.cu header): wide (16 warps,
 // one CTA per SM) and narrow (8 warps, two CTAs per SM).
 namespace wide {
-cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st,
+                          bool reset = true);
 int stage1_ctas_per_sm();
 }  // namespace wide
 namespace narrow {
-cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st);
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st,
+                          bool reset = true);
 int stage1_ctas_per_sm();
 }  // namespace narrow
 int stage1_band_ld();
@@ -56,6 +61,8 @@ struct Stage2Args {
   double* ae;              // per solve: m-1 |off-diagonal|
   long long de_stride;
   int* counter;            // work queue (zeroed before launch)
+  const DevStatus* status; // sticky call status: nonzero code = abort
+  int device;              // for the SM count
 };
 cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st);
 
@@ -73,7 +80,16 @@ struct BisectArgs {
   double* out;           // row r = solve first_solve + r ... see out_ld
   long long out_ld;
   int split;             // CTAs per solve (eigenvalue ranges), >= 1
+  DevStatus* status;     // ConvergenceFailure; nonzero code on entry = abort
+  const double* scale;   // [0] input scale (brackets), [1] its inverse (output); nullable
+  int max_it;            // secant/bisection budget per eigenvalue
 };
+// Exact power-of-two scale of A when max|a_ij| is far outside [2^-400, 2^400]
+// (the reference's tred1 scales every row, eigensolve.cpp:28; the blocked
+// reduction would overflow its column norms instead).  scale[0] = 2^-e,
+// scale[1] = 2^e; both 1 for ordinary inputs, so their results are untouched.
+cudaError_t launch_input_scale(const double* dA, long long count, double* dscale,
+                               cudaStream_t st, int* launches);
 cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
                           cudaStream_t st, int* launches);
 

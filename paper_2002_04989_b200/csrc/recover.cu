@@ -37,49 +37,20 @@ struct RecoverState {
 
 __device__ __forceinline__ double clamp01d(double x) { return fmin(fmax(x, 0.0), 1.0); }
 
-// anchor = argmax mags (first maximum), as signs.cpp:68-70
+// anchor = argmax mags exactly as signs.cpp:68-70 scans it: start at 0 and
+// move on a strict '>' only, so ties keep the first index and a NaN at 0 (or
+// anywhere) never wins or loses a comparison the reference would not.  One
+// thread: n <= 14000 comparisons, negligible next to the LU.
 __global__ void rs_anchor_kernel(const double* mags, int n, RecoverState* st) {
-  __shared__ double sv[kRNT / 32];
-  __shared__ int si[kRNT / 32];
-  double best = -1.0;
-  int bi = 0x7fffffff;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    const double v = mags[j];
-    if (v > best) {  // strided: the first index per thread wins ties
-      best = v;
-      bi = j;
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) {
-      best = ov;
-      bi = oi;
-    }
-  }
-  if (lane == 0) {
-    sv[warp] = best;
-    si[warp] = bi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
-        best = sv[w];
-        bi = si[w];
-      }
-    // NaN magnitudes never win a comparison: fall back to component 0 as
-    // the reference's loop does
-    if (bi == 0x7fffffff) bi = 0;
-    st->anchor = bi;
-    st->singular = 0;
-    st->va = sqrt(clamp01d(mags[bi]));
-    st->res2 = 0.0;
-    st->fro2 = 0.0;
-  }
+  if (threadIdx.x != 0) return;
+  int bi = 0;
+  for (int j = 1; j < n; ++j)
+    if (mags[j] > mags[bi]) bi = j;
+  st->anchor = bi;
+  st->singular = 0;
+  st->va = sqrt(clamp01d(mags[bi]));
+  st->res2 = 0.0;
+  st->fro2 = 0.0;
 }
 
 // W (m x (m+1), ld ldw): B without the anchor row/column | rhs

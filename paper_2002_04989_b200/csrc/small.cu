@@ -109,7 +109,9 @@ __device__ void warp_bisect_all(double* d, double* e2, const double* ae, int m,
   __syncwarp();
   for (int k = lane; k < m; k += 32) {
     d[k] *= sc;
-    if (k + 1 < m) e2[k] *= sc * sc;
+    // (|e| sc)^2, not e^2 sc^2: the same bits for ordinary inputs, and no
+    // overflow of e^2 for entries near 1e300 (tred1 scales its rows)
+    if (k + 1 < m) e2[k] = (ae[k] * sc) * (ae[k] * sc);
   }
   __syncwarp();
   const double fudge = 2.0 * kEps * tn * m + 1e-300;

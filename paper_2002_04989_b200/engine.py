@@ -122,6 +122,15 @@ def seeded_draws(seed: int, count: int, dist: str = "gaussian") -> np.ndarray:
     return out
 
 
+def c3_matrix(n: int = 1024, seed: int = 3) -> np.ndarray:
+    """C3 input: Q diag(linspace(-1, 1)) Q^T, Q the sign-fixed
+    Householder QR factor of a seeded Gaussian matrix, symmetrised; plain
+    deterministic host loops in the C-ABI library (same bytes on any CPU)."""
+    out = np.empty((n, n), np.float64)
+    _native.load().eigenid_c3_matrix(seed, n, _native.dptr(out))
+    return out
+
+
 def c5_lambda(seed: int, n: int) -> np.ndarray:
     """C5 synthetic spectrum: n uniform(-1,1) draws, sorted,
     ties re-drawn from the same stream (strictly increasing)."""
@@ -199,7 +208,7 @@ class Device:
         """ms per stage of the last large-n call (needs set_profiling)."""
         buf = (C.c_double * 5)()
         k = self.lib.eigenid_gpu_stage_times(self.ctx, buf, 5)
-        names = ["stage1", "stage2", "bisect_A", "bisect_minors", "identity"]
+        names = ["stage1", "stage2", "lambda_A", "bisect_minors", "identity"]
         return {names[t]: buf[t] for t in range(k)}
 
     def __del__(self):

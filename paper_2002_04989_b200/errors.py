@@ -79,6 +79,8 @@ _CODES = {
     7: IndexOutOfRange,
     8: SignRecoveryFailure,
     9: DimensionMismatch,
+    10: NonFiniteEntry,
+    11: AsymmetricInput,
 }
 
 

@@ -27,6 +27,8 @@ namespace {
     case EIGENID_E_INDEX: throw IndexOutOfRange(msg);
     case EIGENID_E_SIGN_RECOVERY: throw SignRecoveryFailure(msg);
     case EIGENID_E_DIMENSION: throw DimensionMismatch(msg);
+    case EIGENID_E_NONFINITE_ENTRY: throw NonFiniteEntry(msg);
+    case EIGENID_E_ASYMMETRIC: throw AsymmetricInput(msg);
     default: throw DeviceError(msg, e.cuda_error);
   }
 }
