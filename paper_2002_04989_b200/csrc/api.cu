@@ -96,7 +96,7 @@ struct eigenid_gpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // lambda(A)'s solve, beside the minors
-  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_a0 = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_a0 = nullptr, ev_a1 = nullptr;
   std::mutex mu;
   DevStatus* dstatus = nullptr;
   DevStatus* hstatus = nullptr;  // pinned
@@ -386,6 +386,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   if (identity)
     EID_CUDA(launch_degeneracy(dlam, n, cfg->degeneracy_tol, c->dstatus, sa, &launches),
              "degeneracy");
+  EID_CUDA(cudaEventRecord(c->ev_a1, sa), "event");  // lambda(A) + degeneracy done
   Stage1Args s1{dA, n, djs, cnt0, c->bWs.as<double>(), ws_stride, ldw,
                 c->bBand.as<double>(), band_stride, ctr + 1, c->dstatus, 0, dscale};
   const int grid_main = side_ok ? (cnt0 < slot_a ? cnt0 : slot_a) : (cnt0 < slots ? cnt0 : slots);
@@ -445,7 +446,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   if (timer.on) {  // A's pipeline on the side stream (stage slot 2)
     float ms = 0.f;
     cudaEventSynchronize(c->ev_a);
-    cudaEventElapsedTime(&ms, c->ev_a0, c->ev_a);
+    cudaEventElapsedTime(&ms, c->ev_a0, c->ev_a1);
     timer.side_ms = ms;
   }
   c->launches += launches;
@@ -671,6 +672,7 @@ int eigenid_gpu_create(eigenid_gpu_ctx** out, int device, eigenid_gpu_err* err) 
       (e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreate(&c->ev_a)) != cudaSuccess ||
       (e = cudaEventCreate(&c->ev_a0)) != cudaSuccess ||
+      (e = cudaEventCreate(&c->ev_a1)) != cudaSuccess ||
       (e = cudaMalloc(&c->dstatus, 2 * sizeof(DevStatus))) != cudaSuccess ||
       (e = cudaMallocHost(&c->hstatus, 2 * sizeof(DevStatus))) != cudaSuccess) {
     delete c;
@@ -694,6 +696,7 @@ int eigenid_gpu_destroy(eigenid_gpu_ctx* c) {
   cudaEventDestroy(c->ev_start);
   cudaEventDestroy(c->ev_a);
   cudaEventDestroy(c->ev_a0);
+  cudaEventDestroy(c->ev_a1);
   cudaStreamDestroy(c->side);
   cudaStreamDestroy(c->stream);
   delete c;

@@ -1,5 +1,5 @@
 import sys, time, numpy as np
-sys.path.insert(0, '/root/repo')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.oracle import Oracle
 from paper_2002_04989_b200 import IdentityEngine, IdentityConfig, eigenvalues
 o = Oracle()

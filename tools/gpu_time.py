@@ -1,5 +1,5 @@
 import os, sys, time, numpy as np
-sys.path.insert(0, os.environ.get('GRAFT_REPO_ROOT', '/root/repo'))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ['EIGENID_PROFILE'] = '1'
 from oracle.oracle import Oracle
 from paper_2002_04989_b200 import IdentityEngine
