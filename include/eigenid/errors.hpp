@@ -30,6 +30,15 @@ EIGENID_ERROR(NonFiniteIntermediate)
 EIGENID_ERROR(InternalInconsistency)
 EIGENID_ERROR(ConfigError)
 EIGENID_ERROR(SignRecoveryFailure)
+// The rest of the reference's taxonomy (errors.hpp:36-44, :84-107): thrown
+// by its file I/O, CLI and bench harness (out of scope here); declared so
+// callers' catch clauses compile unchanged.
+EIGENID_ERROR(FileNotFound)
+EIGENID_ERROR(ParseError)
+EIGENID_ERROR(VariantDisagreement)
+EIGENID_ERROR(MissingReference)
+EIGENID_ERROR(IoError)
+EIGENID_ERROR(OracleCapExceeded)
 #undef EIGENID_ERROR
 
 // Repeated eigenvalue of A: components are not unique (errors.hpp:58-66).

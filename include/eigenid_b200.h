@@ -97,6 +97,28 @@ int eigenid_gpu_destroy(eigenid_gpu_ctx* ctx);
 void* eigenid_gpu_stream(eigenid_gpu_ctx* ctx); /* cudaStream_t */
 int eigenid_gpu_sync(eigenid_gpu_ctx* ctx, eigenid_gpu_err* err);
 
+/* Multi-GPU context over devices first_device .. first_device+num_gpus-1 of
+ * this process (one stream per GPU, one NCCL communicator per GPU from
+ * ncclCommInitAll; NCCL is loaded on demand, reusing an already loaded
+ * libnccl.so.2).  eigenid_gpu_all_magnitudes on it shards the minor index j
+ * over the devices (device d owns rows [d n/P, (d+1) n/P)), recomputes
+ * lambda(A) on each, and all-gathers the rows with NCCL before the D2H —
+ * the fan-out the reference runs on its thread pool (identity.cpp:303-314).
+ * The result is bit-identical for every num_gpus.  Other entry points use
+ * the first device. */
+int eigenid_gpu_create_multi(eigenid_gpu_ctx** ctx, int first_device, int num_gpus,
+                             eigenid_gpu_err* err);
+int eigenid_gpu_num_devices(eigenid_gpu_ctx* ctx);
+void* eigenid_gpu_device_stream(eigenid_gpu_ctx* ctx, int d); /* cudaStream_t of device d */
+
+/* Device-resident multi-GPU all_magnitudes: d_a[d] is A (n x n) on device
+ * d, d_out[d] a full n x n buffer on device d; on return (after
+ * eigenid_gpu_sync) every d_out[d] holds the whole matrix (NCCL
+ * all-gather of the per-device rows).  Enqueues only. */
+int eigenid_gpu_all_magnitudes_multi_device(eigenid_gpu_ctx* ctx, const double* const* d_a,
+                                            size_t n, const eigenid_gpu_config* cfg,
+                                            double* const* d_out, eigenid_gpu_err* err);
+
 /* ---- host-pointer entry points (reference-facing) ------------------- */
 
 /* Spectrum eigenvalues(const SymmetricMatrix&)   eigensolve.hpp:46,
@@ -151,6 +173,52 @@ int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* ctx, const double* a,
                                     const eigenid_gpu_config* cfg,
                                     double* value, double* raw, int* method,
                                     eigenid_gpu_err* err);
+
+/* MagnitudeResult (identity.hpp:66-74). */
+typedef struct eigenid_gpu_magnitude {
+  double value;          /* clamped to [0, 1] */
+  double raw_value;      /* pre-clamp */
+  uint64_t i, j;
+  int method;            /* EvaluationMethod: 0 baseline, 1 batched,
+                            2 batched-parallel, 3 log-domain */
+  double condition_flag; /* min |lambda_i - lambda_k| / range */
+} eigenid_gpu_magnitude;
+
+/* The reference's per-component entry points with the full MagnitudeResult:
+ *   variant 0  IdentityEngine::component_magnitude   identity.cpp:240-251
+ *   variant 1  IdentityEngine::log_domain_magnitude  identity.cpp:253-274
+ *   variant 2  component_magnitude_baseline          identity.cpp:151-183
+ *              (natural pairing, running products; EIGENID_E_NONFINITE when
+ *              a product leaves the finite range; always solves)
+ * lambda / mu_j: cached spectra (both or neither; ignored by variant 2). */
+int eigenid_gpu_component(eigenid_gpu_ctx* ctx, const double* a, size_t n, size_t i,
+                          size_t j, const double* lambda, const double* mu_j,
+                          const eigenid_gpu_config* cfg, int variant,
+                          eigenid_gpu_magnitude* out, eigenid_gpu_err* err);
+
+/* IdentityEngine::vector_magnitudes (identity.cpp:276-292) with one
+ * MagnitudeResult per component j (out: n entries). */
+int eigenid_gpu_vector(eigenid_gpu_ctx* ctx, const double* a, size_t n, size_t i,
+                       const eigenid_gpu_config* cfg, eigenid_gpu_magnitude* out,
+                       eigenid_gpu_err* err);
+
+/* log_domain_product (identity.cpp:98-122) of explicit factor lists
+ * (FactorPairing numerator / denominator, len each), on the device. */
+int eigenid_gpu_log_domain_product(eigenid_gpu_ctx* ctx, const double* num,
+                                   const double* den, size_t len, double* out,
+                                   eigenid_gpu_err* err);
+
+/* tridiagonalize (eigensolve.hpp:41): a tridiagonal form orthogonally
+ * similar to A from the device reduction (two-stage, not tred1's sequence:
+ * same eigenvalues, different (diag, offdiag)).  offdiag: n-1 values. */
+int eigenid_gpu_tridiagonalize(eigenid_gpu_ctx* ctx, const double* a, size_t n,
+                               double* diag, double* offdiag, eigenid_gpu_err* err);
+
+/* eigenvalues(TridiagonalForm) (eigensolve.cpp:72-128): ascending
+ * eigenvalues of the given tridiagonal by Sturm bisection on the device. */
+int eigenid_gpu_tridiagonal_eigenvalues(eigenid_gpu_ctx* ctx, const double* diag,
+                                        const double* offdiag, size_t n, double* out,
+                                        eigenid_gpu_err* err);
 
 /* Sign recovery (recover_signs, signs.cpp:48-120; identity.hpp:159-166):
  * the signed eigenvector i from its squared magnitudes (n_magnitudes must

@@ -27,6 +27,12 @@ class GpuConfig(C.Structure):
                 ("log_domain", C.c_int)]
 
 
+class GpuMagnitude(C.Structure):
+    """eigenid_gpu_magnitude = MagnitudeResult (identity.hpp:66-74)."""
+    _fields_ = [("value", C.c_double), ("raw_value", C.c_double), ("i", C.c_uint64),
+                ("j", C.c_uint64), ("method", C.c_int), ("condition_flag", C.c_double)]
+
+
 # every symbol the header declares, with its signature
 SIGNATURES = {
     "eigenid_gpu_abi_version": (C.c_int, []),
@@ -86,6 +92,29 @@ SIGNATURES = {
     "eigenid_seeded_draws": (None, [C.c_uint64, C.c_size_t, C.c_int, _dp]),
     "eigenid_c3_matrix": (None, [C.c_uint64, C.c_size_t, _dp]),
     "eigenid_gpu_set_profiling": (None, [C.c_void_p, C.c_int]),
+    "eigenid_gpu_create_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                           C.POINTER(GpuErr)]),
+    "eigenid_gpu_num_devices": (C.c_int, [C.c_void_p]),
+    "eigenid_gpu_device_stream": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "eigenid_gpu_all_magnitudes_multi_device": (C.c_int, [C.c_void_p,
+                                                          C.POINTER(C.c_void_p),
+                                                          C.c_size_t,
+                                                          C.POINTER(GpuConfig),
+                                                          C.POINTER(C.c_void_p),
+                                                          C.POINTER(GpuErr)]),
+    "eigenid_gpu_component": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t,
+                                        C.c_size_t, _dp, _dp, C.POINTER(GpuConfig),
+                                        C.c_int, C.POINTER(GpuMagnitude),
+                                        C.POINTER(GpuErr)]),
+    "eigenid_gpu_vector": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t,
+                                     C.POINTER(GpuConfig), C.POINTER(GpuMagnitude),
+                                     C.POINTER(GpuErr)]),
+    "eigenid_gpu_log_domain_product": (C.c_int, [C.c_void_p, _dp, _dp, C.c_size_t, _dp,
+                                                 C.POINTER(GpuErr)]),
+    "eigenid_gpu_tridiagonalize": (C.c_int, [C.c_void_p, _dp, C.c_size_t, _dp, _dp,
+                                             C.POINTER(GpuErr)]),
+    "eigenid_gpu_tridiagonal_eigenvalues": (C.c_int, [C.c_void_p, _dp, _dp, C.c_size_t,
+                                                      _dp, C.POINTER(GpuErr)]),
     "eigenid_gpu_stage_times": (C.c_int, [C.c_void_p, _dp, C.c_int]),
 }
 

@@ -20,6 +20,7 @@ LIB = os.path.join(PKG, "libeigenid_b200.so")
 HOSTLIB = os.path.join(PKG, "libeigenid.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+REFERENCE = os.environ.get("EIGENID_REFERENCE", "/root/reference/proj")
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -56,6 +57,21 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared",
               "-I" + os.path.join(ROOT, "include"), *hsrc, "-o", HOSTLIB,
               "-L" + PKG, "-leigenid_b200", "-Wl,-rpath,$ORIGIN", "-pthread"])
+    # The reference's own acceptance suite against the drop-in headers
+    # (tests/cpp/acceptance_shim.cpp supplies the reference's Jacobi oracle
+    # from oracle/_ref).  Only where /root/reference exists; the binary ships
+    # to the GPU box with the snapshot.
+    acc_src = os.path.join(REFERENCE, "tests", "acceptance.cpp")
+    acc_bin = os.path.join(ROOT, "tests", "cpp", "acceptance")
+    shim = os.path.join(ROOT, "tests", "cpp", "acceptance_shim.cpp")
+    ref_so = os.path.join(ROOT, "oracle", "_ref", "libeigenid_ref.so")
+    if os.path.exists(acc_src) and os.path.exists(ref_so) and (
+            force or _newer(acc_bin, [acc_src, shim, HOSTLIB, ref_so])):
+        _run(["g++", "-O2", "-std=gnu++20", "-I" + os.path.join(ROOT, "include"),
+              "-I" + os.path.join(REFERENCE, "include"), acc_src, shim, "-o", acc_bin,
+              "-L" + PKG, "-leigenid", "-leigenid_b200",
+              "-L" + os.path.dirname(ref_so), "-leigenid_ref",
+              "-Wl,-rpath," + PKG + ":" + os.path.dirname(ref_so), "-pthread"])
     test_src = os.path.join(ROOT, "tests", "cpp", "test_host.cpp")
     test_bin = os.path.join(ROOT, "tests", "cpp", "test_host")
     if os.path.exists(test_src) and (force or _newer(test_bin, [test_src, HOSTLIB])):

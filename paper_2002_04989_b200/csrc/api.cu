@@ -13,6 +13,8 @@
 // status record into the reference's typed errors.  There is no CPU
 // fallback: without a device every entry point returns EIGENID_E_DEVICE.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is loaded on demand (see NcclApi)
 
 #include <atomic>
 #include <cmath>
@@ -110,6 +112,12 @@ struct eigenid_gpu_ctx {
   std::atomic<uint64_t> launches{0};
   bool profiling = false;
   double stage_ms[5] = {0, 0, 0, 0, 0};
+  // multi-device context (eigenid_gpu_create_multi): peer[0] == this, one
+  // single-device context per further GPU, one NCCL communicator per GPU
+  int ngpu = 1;
+  bool multi = false;  // created by eigenid_gpu_create_multi (NCCL path, any P)
+  eigenid_gpu_ctx* peer[8] = {};
+  ncclComm_t comm[8] = {};
 };
 
 namespace {
@@ -227,6 +235,49 @@ int check_finite(eigenid_gpu_ctx* c, const double* dA, size_t per, size_t count,
   EID_CUDA(cudaGetLastError(), "nonfinite check");
   c->launches += 1;
   return EIGENID_OK;
+}
+
+// NCCL, resolved at run time: the process may already hold the NCCL that
+// PyTorch ships (libnccl.so.2 of nvidia-nccl), which is then reused
+// (RTLD_NOLOAD); otherwise the system libnccl.so.2 is loaded.  Only
+// multi-device contexts need it, so single-GPU users never load NCCL.
+struct NcclApi {
+  ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.comm_init_all = reinterpret_cast<decltype(a.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(h, "ncclBroadcast"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.comm_init_all && a.comm_destroy && a.all_gather && a.broadcast &&
+           a.group_start && a.group_end && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+int nccl_fail(eigenid_gpu_err* err, ncclResult_t r, const char* where) {
+  set_err(err, EIGENID_E_DEVICE, -1, 0.0, 0,
+          std::string(where) + ": " + (nccl().error_string ? nccl().error_string(r) : "?"));
+  return EIGENID_E_DEVICE;
 }
 
 // Per-stage device timing of run_large: enabled per context through
@@ -377,7 +428,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
                  dscale};
   EID_CUDA(launch1(s1a, 1, sa, true), "stage1 A");
   Stage2Args s2a{c->bBandA.as<double>(), band_stride, djsA, 1, n, dA_d, dA_d + n,
-                 dA_d + 2 * n, n, ctr + 3, c->dstatus, c->device};
+                 dA_d + 2 * n, n, ctr + 3, c->dstatus, c->device, cps > 1 ? 1 : 0};
   EID_CUDA(launch_stage2(s2a, sa), "stage2 A");
   BisectArgs ba{dA_d, dA_d + n, dA_d + 2 * n, n, djsA, 1, 0, n, nullptr, dlam, n,
                 (n + 255) / 256, c->dstatus, dscale, max_it};
@@ -502,6 +553,136 @@ int identity_impl(eigenid_gpu_ctx* c, const double* d_lambda,
                   const double* d_mu, size_t n, size_t j0, size_t j1,
                   const eigenid_gpu_config* cfg, double* d_out,
                   eigenid_gpu_err* err);
+
+// Minor index j sharded over the devices of a multi-device context
+// (SURVEY §8 e): device d owns the contiguous rows [d n / P, (d+1) n / P) of
+// out[j*n+i], recomputes lambda(A) (1/n of the work) and writes its rows into
+// its own full n x n buffer; one NCCL all-gather (in place; per-root
+// broadcasts when P does not divide n) then leaves the whole matrix on every
+// device.  Each (i, j) is computed by the same per-solve kernels whatever P
+// is, so the result is bit-identical for every device count.
+void shard_of(size_t n, int P, int d, size_t* j0, size_t* j1) {
+  *j0 = n * (size_t)d / (size_t)P;
+  *j1 = n * (size_t)(d + 1) / (size_t)P;
+}
+
+int multi_enqueue(eigenid_gpu_ctx* c, const double* const* dA, size_t n,
+                  const eigenid_gpu_config* cfg, double* const* dfull,
+                  double* const* dlam, double* const* dmu, eigenid_gpu_err* err) {
+  const int P = c->ngpu;
+  for (int d = 0; d < P; ++d) {
+    eigenid_gpu_ctx* p = c->peer[d];
+    size_t j0, j1;
+    shard_of(n, P, d, &j0, &j1);
+    int st;
+    if ((st = begin(p, err))) return st;
+    p->pending = true;
+    if ((st = check_finite(p, dA[d], n * n, 1, err))) return st;
+    if ((st = run_all(p, dA[d], (int)n, (int)j0, (int)j1, cfg, dfull[d] + j0 * n, dlam[d],
+                      dmu[d], err)))
+      return st;
+  }
+  if (!c->multi) return EIGENID_OK;  // a single-device context: nothing to gather
+  const NcclApi& api = nccl();
+  ncclResult_t r = api.group_start();
+  if (r != ncclSuccess) return nccl_fail(err, r, "ncclGroupStart");
+  if (n % (size_t)P == 0) {
+    const size_t cnt = n / P * n;
+    for (int d = 0; d < P; ++d) {
+      EID_CUDA(cudaSetDevice(c->peer[d]->device), "cudaSetDevice");
+      r = api.all_gather(dfull[d] + (size_t)d * cnt, dfull[d], cnt, ncclFloat64, c->comm[d],
+                         c->peer[d]->stream);
+      if (r != ncclSuccess) {
+        api.group_end();
+        return nccl_fail(err, r, "ncclAllGather");
+      }
+    }
+  } else {
+    for (int root = 0; root < P; ++root) {
+      size_t j0, j1;
+      shard_of(n, P, root, &j0, &j1);
+      for (int d = 0; d < P; ++d) {
+        EID_CUDA(cudaSetDevice(c->peer[d]->device), "cudaSetDevice");
+        r = api.broadcast(dfull[d] + j0 * n, dfull[d] + j0 * n, (j1 - j0) * n, ncclFloat64,
+                          root, c->comm[d], c->peer[d]->stream);
+        if (r != ncclSuccess) {
+          api.group_end();
+          return nccl_fail(err, r, "ncclBroadcast");
+        }
+      }
+    }
+  }
+  r = api.group_end();
+  if (r != ncclSuccess) return nccl_fail(err, r, "ncclGroupEnd");
+  return EIGENID_OK;
+}
+
+// Reads every device's status (first failing device wins).
+int multi_finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
+  int first = EIGENID_OK;
+  for (int d = 0; d < c->ngpu; ++d) {
+    eigenid_gpu_err e{};
+    bool dg = false;
+    EID_CUDA(cudaSetDevice(c->peer[d]->device), "cudaSetDevice");
+    const int st = finish(c->peer[d], &e, &dg);
+    if (st && first == EIGENID_OK) {
+      first = st;
+      if (err) *err = e;
+      if (degenerate) *degenerate = dg;
+    }
+  }
+  return first;
+}
+
+int all_magnitudes_multi(eigenid_gpu_ctx* c, const double* a, size_t n,
+                         const eigenid_gpu_config* cfg, double* out, double* lambda_out,
+                         double* mu_out, eigenid_gpu_err* err) {
+  const int P = c->ngpu;
+  const double* dA[8];
+  double* dfull[8];
+  double* dlam[8];
+  double* dmu[8];
+  for (int d = 0; d < P; ++d) {
+    eigenid_gpu_ctx* p = c->peer[d];
+    size_t j0, j1;
+    shard_of(n, P, d, &j0, &j1);
+    EID_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+    EID_CUDA(p->bA.ensure(sizeof(double) * n * n), "alloc A");
+    EID_CUDA(p->bOut.ensure(sizeof(double) * n * n), "alloc out");
+    EID_CUDA(p->bLam.ensure(sizeof(double) * n), "alloc lam");
+    EID_CUDA(p->bMu.ensure(sizeof(double) * (j1 > j0 ? j1 - j0 : 1) * (n - 1)), "alloc mu");
+    EID_CUDA(cudaMemcpyAsync(p->bA.p, a, sizeof(double) * n * n, cudaMemcpyHostToDevice,
+                             p->stream), "H2D A");
+    dA[d] = p->bA.as<double>();
+    dfull[d] = p->bOut.as<double>();
+    dlam[d] = p->bLam.as<double>();
+    dmu[d] = p->bMu.as<double>();
+  }
+  int st = multi_enqueue(c, dA, n, cfg, dfull, dlam, dmu, err);
+  if (st) return st;
+  EID_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  EID_CUDA(cudaMemcpyAsync(out, dfull[0], sizeof(double) * n * n, cudaMemcpyDeviceToHost,
+                           c->stream), "D2H out");
+  if (lambda_out)
+    EID_CUDA(cudaMemcpyAsync(lambda_out, dlam[0], sizeof(double) * n,
+                             cudaMemcpyDeviceToHost, c->stream), "D2H lambda");
+  if (mu_out)
+    for (int d = 0; d < P; ++d) {
+      size_t j0, j1;
+      shard_of(n, P, d, &j0, &j1);
+      if (j1 == j0) continue;
+      EID_CUDA(cudaSetDevice(c->peer[d]->device), "cudaSetDevice");
+      EID_CUDA(cudaMemcpyAsync(mu_out + j0 * (n - 1), dmu[d],
+                               sizeof(double) * (j1 - j0) * (n - 1), cudaMemcpyDeviceToHost,
+                               c->peer[d]->stream), "D2H mu");
+    }
+  bool degenerate = false;
+  st = multi_finish(c, err, &degenerate);
+  c->solves += st == EIGENID_E_NONFINITE_ENTRY
+                   ? 0
+                   : ((st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1);
+  return st;
+}
 
 int check_n(size_t n, eigenid_gpu_err* err) {
   if (n < 2) {  // identity.cpp:296-297
@@ -665,6 +846,7 @@ int eigenid_gpu_create(eigenid_gpu_ctx** out, int device, eigenid_gpu_err* err) 
     return EIGENID_E_ALLOC;
   }
   c->device = device;
+  c->peer[0] = c;
   if ((e = cudaSetDevice(device)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) !=
           cudaSuccess ||
@@ -682,8 +864,65 @@ int eigenid_gpu_create(eigenid_gpu_ctx** out, int device, eigenid_gpu_err* err) 
   return EIGENID_OK;
 }
 
+int eigenid_gpu_create_multi(eigenid_gpu_ctx** out, int first_device, int num_gpus,
+                             eigenid_gpu_err* err) {
+  if (!out) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "null ctx pointer");
+    return EIGENID_E_CONFIG;
+  }
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+  if (num_gpus < 1 || num_gpus > 8 || first_device < 0 || first_device + num_gpus > count) {
+    set_err(err, num_gpus < 1 || num_gpus > 8 ? EIGENID_E_CONFIG : EIGENID_E_DEVICE, -1, 0.0,
+            0, "num_gpus must be 1..8 and every device must exist");
+    return num_gpus < 1 || num_gpus > 8 ? EIGENID_E_CONFIG : EIGENID_E_DEVICE;
+  }
+  if (!nccl().ok) {
+    set_err(err, EIGENID_E_DEVICE, -1, 0.0, 0, "libnccl.so.2 could not be loaded");
+    return EIGENID_E_DEVICE;
+  }
+  eigenid_gpu_ctx* c = nullptr;
+  int st = eigenid_gpu_create(&c, first_device, err);
+  if (st) return st;
+  c->ngpu = num_gpus;
+  c->multi = true;
+  c->peer[0] = c;
+  for (int d = 1; d < num_gpus; ++d) {
+    if ((st = eigenid_gpu_create(&c->peer[d], first_device + d, err))) {
+      eigenid_gpu_destroy(c);
+      return st;
+    }
+  }
+  int devs[8];
+  for (int d = 0; d < num_gpus; ++d) devs[d] = first_device + d;
+  const ncclResult_t r = nccl().comm_init_all(c->comm, num_gpus, devs);
+  if (r != ncclSuccess) {
+    for (int d = 0; d < 8; ++d) c->comm[d] = nullptr;
+    eigenid_gpu_destroy(c);
+    return nccl_fail(err, r, "ncclCommInitAll");
+  }
+  *out = c;
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_num_devices(eigenid_gpu_ctx* c) { return c ? c->ngpu : 0; }
+
+void* eigenid_gpu_device_stream(eigenid_gpu_ctx* c, int d) {
+  if (!c || d < 0 || d >= c->ngpu) return nullptr;
+  return (void*)c->peer[d]->stream;
+}
+
 int eigenid_gpu_destroy(eigenid_gpu_ctx* c) {
   if (!c) return EIGENID_OK;
+  if (c->multi) {
+    for (int d = 0; d < c->ngpu; ++d) {
+      if (c->comm[d]) nccl().comm_destroy(c->comm[d]);
+      c->comm[d] = nullptr;
+    }
+    for (int d = 1; d < c->ngpu; ++d) eigenid_gpu_destroy(c->peer[d]);
+    c->ngpu = 1;
+  }
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->bA, &c->bOut, &c->bLam, &c->bMu, &c->bDen, &c->bRcp,
@@ -707,12 +946,42 @@ void* eigenid_gpu_stream(eigenid_gpu_ctx* c) { return c ? (void*)c->stream : nul
 
 int eigenid_gpu_sync(eigenid_gpu_ctx* c, eigenid_gpu_err* err) {
   std::lock_guard<std::mutex> g(c->mu);
+  if (c->multi) return multi_finish(c, err, nullptr);
   return finish(c, err, nullptr);
+}
+
+int eigenid_gpu_all_magnitudes_multi_device(eigenid_gpu_ctx* c, const double* const* d_a,
+                                            size_t n, const eigenid_gpu_config* cfg,
+                                            double* const* d_out, eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  const int P = c->ngpu;
+  double* dlam[8];
+  double* dmu[8];
+  for (int d = 0; d < P; ++d) {
+    eigenid_gpu_ctx* p = c->peer[d];
+    size_t j0, j1;
+    shard_of(n, P, d, &j0, &j1);
+    EID_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+    EID_CUDA(p->bLam.ensure(sizeof(double) * n), "alloc lam");
+    EID_CUDA(p->bMu.ensure(sizeof(double) * (j1 > j0 ? j1 - j0 : 1) * (n - 1)), "alloc mu");
+    dlam[d] = p->bLam.as<double>();
+    dmu[d] = p->bMu.as<double>();
+  }
+  st = multi_enqueue(c, d_a, n, cfg, d_out, dlam, dmu, err);
+  if (st == EIGENID_OK) c->solves += n + 1;
+  return st;
 }
 
 size_t eigenid_gpu_solve_count(eigenid_gpu_ctx* c) { return c->solves.load(); }
 void eigenid_gpu_reset_solve_count(eigenid_gpu_ctx* c) { c->solves.store(0); }
-uint64_t eigenid_gpu_launch_count(eigenid_gpu_ctx* c) { return c->launches.load(); }
+uint64_t eigenid_gpu_launch_count(eigenid_gpu_ctx* c) {
+  uint64_t t = c->launches.load();
+  for (int d = 1; d < c->ngpu; ++d) t += c->peer[d]->launches.load();
+  return t;
+}
 
 void eigenid_gpu_set_profiling(eigenid_gpu_ctx* c, int on) { c->profiling = on != 0; }
 
@@ -762,6 +1031,7 @@ int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
   if (st) return st;
   if ((st = check_cfg(cfg, err))) return st;
   std::lock_guard<std::mutex> g(c->mu);
+  if (c->multi) return all_magnitudes_multi(c, a, n, cfg, out, lambda_out, mu_out, err);
   if ((st = begin(c, err))) return st;
   const size_t nn = n * n;
   EID_CUDA(c->bA.ensure(sizeof(double) * nn), "alloc A");
@@ -1008,14 +1278,19 @@ int eigenid_gpu_all_magnitudes_batched_device(eigenid_gpu_ctx* c,
   return EIGENID_OK;
 }
 
-int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
-                                  size_t n, size_t i,
-                                  const eigenid_gpu_config* cfg, double* out,
-                                  double* out_raw, eigenid_gpu_err* err) {
+}  // extern "C"
+
+namespace {
+// vector_magnitudes (identity.cpp:276-292): lambda(A), the n minor spectra,
+// check_nondegenerate(i), then evaluate() for every j.  raw / method (n
+// each) and the condition flag of eigenvalue i.
+int vector_impl(eigenid_gpu_ctx* c, const double* a, size_t n, size_t i,
+                const eigenid_gpu_config* cfg, std::vector<double>& raw,
+                std::vector<double>& method, double* cond, eigenid_gpu_err* err) {
   int st = check_n(n, err);
   if (st) return st;
   if ((st = check_cfg(cfg, err))) return st;
-  if (i >= n) {
+  if (i >= n) {  // check_component_indices(a, i, 0), identity.cpp:28-36
     set_err(err, EIGENID_E_INDEX, (long long)i, 0.0, 0, "component index out of range");
     return EIGENID_E_INDEX;
   }
@@ -1024,7 +1299,7 @@ int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
   EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
   EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
   EID_CUDA(c->bMu.ensure(sizeof(double) * n * (n - 1)), "alloc mu");
-  EID_CUDA(c->bOut.ensure(sizeof(double) * n), "alloc out");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * (2 * n + 4)), "alloc out");
   EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n,
                            cudaMemcpyHostToDevice, c->stream), "H2D A");
   if ((st = check_finite(c, c->bA.as<double>(), n * n, 1, err))) return st;
@@ -1033,27 +1308,184 @@ int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
                  c->bLam.as<double>(), c->bMu.as<double>(), false, err);
   if (st) return st;
   int launches = 0;
-  // check_nondegenerate for eigenvalue i (identity.cpp:137-139, :281)
+  double* dout = c->bOut.as<double>();
+  // check_nondegenerate for eigenvalue i (identity.cpp:137-139, :281) and
+  // its condition flag (component (i, 0) evaluated into the tail)
   EID_CUDA(launch_component(c->bLam.as<double>(), c->bMu.as<double>(), (int)n,
                             (int)i, batch_of(cfg, (int)n), cfg->degeneracy_tol,
-                            cfg->log_domain, c->bOut.as<double>(), c->dstatus,
+                            cfg->log_domain, 0, dout + 2 * n, c->dstatus,
                             c->stream, &launches), "gap check");
   EID_CUDA(launch_vector(c->bLam.as<double>(), c->bMu.as<double>(), (int)n,
-                         (int)i, batch_of(cfg, (int)n), c->bOut.as<double>(),
+                         (int)i, batch_of(cfg, (int)n), cfg->log_domain, dout, dout + n,
                          c->dstatus, c->stream, &launches), "vector");
   c->launches += launches;
-  std::vector<double> raw(n);
-  EID_CUDA(cudaMemcpyAsync(raw.data(), c->bOut.p, sizeof(double) * n,
+  std::vector<double> h(2 * n + 4);
+  EID_CUDA(cudaMemcpyAsync(h.data(), dout, sizeof(double) * (2 * n + 4),
                            cudaMemcpyDeviceToHost, c->stream), "D2H");
   bool degenerate = false;
   st = finish(c, err, &degenerate);
-  c->solves += (st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1;
+  c->solves += st == EIGENID_E_NONFINITE_ENTRY
+                   ? 0
+                   : ((st == EIGENID_E_DEGENERATE && degenerate) ? 1 : n + 1);
+  if (st) return st;
+  raw.assign(h.begin(), h.begin() + n);
+  method.assign(h.begin() + n, h.begin() + 2 * n);
+  *cond = h[2 * n + 3];
+  return EIGENID_OK;
+}
+
+inline double clamp01h(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }
+}  // namespace
+
+extern "C" {
+
+int eigenid_gpu_vector_magnitudes(eigenid_gpu_ctx* c, const double* a,
+                                  size_t n, size_t i,
+                                  const eigenid_gpu_config* cfg, double* out,
+                                  double* out_raw, eigenid_gpu_err* err) {
+  std::vector<double> raw, method;
+  double cond = 0.0;
+  const int st = vector_impl(c, a, n, i, cfg, raw, method, &cond, err);
   if (st) return st;
   for (size_t t = 0; t < n; ++t) {
-    out[t] = raw[t] < 0.0 ? 0.0 : (1.0 < raw[t] ? 1.0 : raw[t]);
+    out[t] = clamp01h(raw[t]);
     if (out_raw) out_raw[t] = raw[t];
   }
   return EIGENID_OK;
+}
+
+int eigenid_gpu_vector(eigenid_gpu_ctx* c, const double* a, size_t n, size_t i,
+                       const eigenid_gpu_config* cfg, eigenid_gpu_magnitude* out,
+                       eigenid_gpu_err* err) {
+  std::vector<double> raw, method;
+  double cond = 0.0;
+  const int st = vector_impl(c, a, n, i, cfg, raw, method, &cond, err);
+  if (st) return st;
+  for (size_t t = 0; t < n; ++t) {
+    out[t].value = clamp01h(raw[t]);
+    out[t].raw_value = raw[t];
+    out[t].i = i;
+    out[t].j = t;
+    out[t].method = (int)method[t];
+    out[t].condition_flag = cond;
+  }
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_log_domain_product(eigenid_gpu_ctx* c, const double* num,
+                                   const double* den, size_t len, double* out,
+                                   eigenid_gpu_err* err) {
+  std::lock_guard<std::mutex> g(c->mu);
+  int st;
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bOut.ensure(sizeof(double) * (2 * len + 2)), "alloc factors");
+  double* d = c->bOut.as<double>();
+  if (len) {
+    EID_CUDA(cudaMemcpyAsync(d, num, sizeof(double) * len, cudaMemcpyHostToDevice,
+                             c->stream), "H2D num");
+    EID_CUDA(cudaMemcpyAsync(d + len, den, sizeof(double) * len,
+                             cudaMemcpyHostToDevice, c->stream), "H2D den");
+  }
+  int launches = 0;
+  EID_CUDA(launch_log_product(d, d + len, (long long)len, d + 2 * len, c->dstatus,
+                              c->stream, &launches), "log product");
+  c->launches += launches;
+  double h = 0.0;
+  EID_CUDA(cudaMemcpyAsync(&h, d + 2 * len, sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream), "D2H");
+  if ((st = finish(c, err, nullptr))) {
+    if (st == EIGENID_E_DEGENERATE)
+      set_err(err, st, -1, 0.0, 0, "zero denominator factor");  // identity.cpp:110
+    return st;
+  }
+  *out = h;
+  return EIGENID_OK;
+}
+
+// tridiagonalize (eigensolve.hpp:41): the device reduction (dense -> band ->
+// tridiagonal) of A; an orthogonally similar tridiagonal, not tred1's own.
+int eigenid_gpu_tridiagonalize(eigenid_gpu_ctx* c, const double* a, size_t n,
+                               double* diag, double* offdiag, eigenid_gpu_err* err) {
+  if (n < 1) {
+    set_err(err, EIGENID_E_DIMENSION, -1, 0.0, 0, "matrix dimension must be >= 1");
+    return EIGENID_E_DIMENSION;
+  }
+  if (n > (size_t)kLargeMax) return check_n(n, err);
+  if (n == 1) {
+    diag[0] = a[0];
+    return EIGENID_OK;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  int st;
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bA.ensure(sizeof(double) * n * n), "alloc A");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * 2 * n), "alloc out");
+  EID_CUDA(cudaMemcpyAsync(c->bA.p, a, sizeof(double) * n * n, cudaMemcpyHostToDevice,
+                           c->stream), "H2D A");
+  if ((st = check_finite(c, c->bA.as<double>(), n * n, 1, err))) return st;
+  eigenid_gpu_config cfg{64, 0.0, 0};
+  st = run_large(c, c->bA.as<double>(), (int)n, 0, 0, &cfg, nullptr,
+                 c->bLam.as<double>(), nullptr, false, err);
+  if (st) return st;
+  int launches = 0;
+  // the chased band of A holds (d, e) scaled by the exact input scale
+  EID_CUDA(launch_band_tridiag(c->bBandA.as<double>(), stage1_band_ld(), (int)n,
+                               c->bOut.as<double>(), c->bOut.as<double>() + n, c->stream,
+                               &launches), "band tridiag");
+  c->launches += launches;
+  std::vector<double> h(2 * n), sc(2);
+  EID_CUDA(cudaMemcpyAsync(h.data(), c->bOut.p, sizeof(double) * 2 * n,
+                           cudaMemcpyDeviceToHost, c->stream), "D2H");
+  EID_CUDA(cudaMemcpyAsync(sc.data(), c->bScale.p, sizeof(double) * 2,
+                           cudaMemcpyDeviceToHost, c->stream), "D2H scale");
+  if ((st = finish(c, err, nullptr))) return st;
+  for (size_t k = 0; k < n; ++k) diag[k] = h[k] * sc[1];
+  for (size_t k = 0; k + 1 < n; ++k) offdiag[k] = h[n + k] * sc[1];
+  return EIGENID_OK;
+}
+
+// eigenvalues(TridiagonalForm) (eigensolve.cpp:72-128): Sturm bisection of
+// the given (diag, offdiag) on the device, ascending.
+int eigenid_gpu_tridiagonal_eigenvalues(eigenid_gpu_ctx* c, const double* diag,
+                                        const double* offdiag, size_t n, double* out,
+                                        eigenid_gpu_err* err) {
+  if (n == 0) return EIGENID_OK;
+  if (n > (size_t)kLargeMax) return check_n(n, err);
+  if (n == 1) {
+    out[0] = diag[0];
+    return EIGENID_OK;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  int st;
+  if ((st = begin(c, err))) return st;
+  EID_CUDA(c->bOut.ensure(sizeof(double) * 2 * n), "alloc de");
+  EID_CUDA(c->bDeA.ensure(sizeof(double) * 3 * n), "alloc deA");
+  EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc out");
+  EID_CUDA(c->bJsA.ensure(sizeof(int)), "alloc js");
+  EID_CUDA(c->bScale.ensure(sizeof(double) * 4), "alloc scale");
+  double* de = c->bOut.as<double>();
+  EID_CUDA(cudaMemcpyAsync(de, diag, sizeof(double) * n, cudaMemcpyHostToDevice,
+                           c->stream), "H2D d");
+  EID_CUDA(cudaMemcpyAsync(de + n, offdiag, sizeof(double) * (n - 1),
+                           cudaMemcpyHostToDevice, c->stream), "H2D e");
+  EID_CUDA(cudaMemsetAsync(c->bJsA.p, 0xff, sizeof(int), c->stream), "js");
+  int launches = 0;
+  double* dscale = c->bScale.as<double>();
+  EID_CUDA(launch_input_scale(de, 2LL * n - 1, dscale, c->stream, &launches), "scale");
+  double* d3 = c->bDeA.as<double>();
+  EID_CUDA(launch_tridiag_prepare(de, (int)n, dscale, d3, d3 + n, d3 + 2 * n, c->stream,
+                                  &launches), "prepare");
+  int max_it = 300;
+  if (const char* mi = std::getenv("EIGENID_BISECT_MAX_IT")) max_it = std::atoi(mi);
+  BisectArgs ba{d3, d3 + n, d3 + 2 * n, (long long)n, c->bJsA.as<int>(), 1, 0, (int)n,
+                nullptr, c->bLam.as<double>(), (long long)n, (int)((n + 255) / 256),
+                c->dstatus, dscale, max_it};
+  EID_CUDA(launch_bisect(ba, 1, (int)n, c->stream, &launches), "bisect");
+  c->launches += launches;
+  EID_CUDA(cudaMemcpyAsync(out, c->bLam.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                           c->stream), "D2H");
+  return finish(c, err, nullptr);
 }
 
 // ---- sign recovery (signs.cpp:48-120) ------------------------------------
@@ -1134,26 +1566,36 @@ int eigenid_gpu_recover_signs_device(eigenid_gpu_ctx* c, const double* d_a, size
   return recover_impl(c, d_a, n, d_magnitudes, lambda_i, sign_tol, d_out, err);
 }
 
-int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* c, const double* a,
-                                    size_t n, size_t i, size_t j,
-                                    const double* lambda, const double* mu_j,
-                                    const eigenid_gpu_config* cfg,
-                                    double* value, double* raw, int* method,
-                                    eigenid_gpu_err* err) {
+}  // extern "C"
+
+namespace {
+// One component through the reference's per-component entries
+// (identity.cpp:151-183 baseline, :240-251 component_magnitude, :253-274
+// log_domain_magnitude).  Cached spectra (lambda and mu_j both given) skip
+// the two solves; the baseline always solves, as the reference's does.
+// out4 = {value, raw, method, condition_flag}.
+int component_impl(eigenid_gpu_ctx* c, const double* a, size_t n, size_t i,
+                   size_t j, const double* lambda, const double* mu_j,
+                   const eigenid_gpu_config* cfg, int variant, double* out4,
+                   eigenid_gpu_err* err) {
   if (n < 2) return check_n(n, err);
   int st = check_cfg(cfg, err);
   if (st) return st;
   if (i >= n || j >= n) {  // check_component_indices, identity.cpp:28-36
-    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, "component index out of range");
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "component index (i=%zu, j=%zu) out of range for n = %zu",
+                  i, j, n);
+    set_err(err, EIGENID_E_INDEX, -1, 0.0, 0, buf);
     return EIGENID_E_INDEX;
   }
+  const bool cached = lambda && mu_j && variant != 2;
   std::lock_guard<std::mutex> g(c->mu);
   if ((st = begin(c, err))) return st;
   EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
   EID_CUDA(c->bMu.ensure(sizeof(double) * n), "alloc mu");
   EID_CUDA(c->bOut.ensure(sizeof(double) * 4), "alloc out");
   size_t solves = 0;
-  if (lambda && mu_j) {
+  if (cached) {
     EID_CUDA(cudaMemcpyAsync(c->bLam.p, lambda, sizeof(double) * n,
                              cudaMemcpyHostToDevice, c->stream), "H2D lambda");
     EID_CUDA(cudaMemcpyAsync(c->bMu.p, mu_j, sizeof(double) * (n - 1),
@@ -1172,20 +1614,61 @@ int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* c, const double* a,
     solves = 2;
   }
   int launches = 0;
+  const int logd = variant == 1 ? 1 : cfg->log_domain;
   EID_CUDA(launch_component(c->bLam.as<double>(), c->bMu.as<double>(), (int)n,
                             (int)i, batch_of(cfg, (int)n), cfg->degeneracy_tol,
-                            cfg->log_domain, c->bOut.as<double>(), c->dstatus,
+                            logd, variant, c->bOut.as<double>(), c->dstatus,
                             c->stream, &launches), "component");
   c->launches += launches;
-  double h[3];
-  EID_CUDA(cudaMemcpyAsync(h, c->bOut.p, sizeof(double) * 3,
+  EID_CUDA(cudaMemcpyAsync(out4, c->bOut.p, sizeof(double) * 4,
                            cudaMemcpyDeviceToHost, c->stream), "D2H");
   st = finish(c, err, nullptr);
-  c->solves += solves;
+  c->solves += st == EIGENID_E_NONFINITE_ENTRY ? 0 : solves;
+  if (st == EIGENID_E_NONFINITE) {
+    static const char* what[4] = {"", "numerator product left the finite range",
+                                  "denominator product left the finite range",
+                                  "factor ratio is not finite"};  // identity.cpp:163-174
+    const long long k = c->hstatus[0].aux;
+    set_err(err, st, -1, 0.0, 0, what[k >= 1 && k <= 3 ? k : 3]);
+  }
+  return st;
+}
+}  // namespace
+
+extern "C" {
+
+int eigenid_gpu_component_magnitude(eigenid_gpu_ctx* c, const double* a,
+                                    size_t n, size_t i, size_t j,
+                                    const double* lambda, const double* mu_j,
+                                    const eigenid_gpu_config* cfg,
+                                    double* value, double* raw, int* method,
+                                    eigenid_gpu_err* err) {
+  double h[4];
+  const int st = component_impl(c, a, n, i, j, lambda, mu_j, cfg, 0, h, err);
   if (st) return st;
   *value = h[0];
   if (raw) *raw = h[1];
   if (method) *method = (int)h[2];
+  return EIGENID_OK;
+}
+
+int eigenid_gpu_component(eigenid_gpu_ctx* c, const double* a, size_t n, size_t i,
+                          size_t j, const double* lambda, const double* mu_j,
+                          const eigenid_gpu_config* cfg, int variant,
+                          eigenid_gpu_magnitude* out, eigenid_gpu_err* err) {
+  if (variant < 0 || variant > 2) {
+    set_err(err, EIGENID_E_CONFIG, -1, 0.0, 0, "unknown component variant");
+    return EIGENID_E_CONFIG;
+  }
+  double h[4];
+  const int st = component_impl(c, a, n, i, j, lambda, mu_j, cfg, variant, h, err);
+  if (st) return st;
+  out->value = h[0];
+  out->raw_value = h[1];
+  out->i = i;
+  out->j = j;
+  out->method = (int)h[2];
+  out->condition_flag = h[3];
   return EIGENID_OK;
 }
 

@@ -306,6 +306,43 @@ cudaError_t launch_input_scale(const double* dA, long long count, double* dscale
   return cudaGetLastError();
 }
 
+// Signed tridiagonal of a band after the chase: d_k = AB[k][0], e_k = AB[k][1].
+__global__ void band_tridiag_kernel(const double* __restrict__ band, int ldab, int n,
+                                    double* d, double* e) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    d[k] = band[(long long)k * ldab];
+    if (k + 1 < n) e[k] = band[(long long)k * ldab + 1];
+  }
+}
+cudaError_t launch_band_tridiag(const double* band, int ldab, int n, double* d,
+                                double* e, cudaStream_t st, int* launches) {
+  band_tridiag_kernel<<<(n + 255) / 256, 256, 0, st>>>(band, ldab, n, d, e);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// de = [d (n) | e (n-1)] -> d*s, (|e| s)^2, |e| s with the exact input scale.
+__global__ void tridiag_prepare_kernel(const double* __restrict__ de, int n,
+                                       const double* scale, double* d, double* e2,
+                                       double* ae) {
+  const double s = scale[0];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    d[k] = de[k] * s;
+    if (k + 1 < n) {
+      const double a = fabs(de[n + k]) * s;
+      ae[k] = a;
+      e2[k] = a * a;
+    }
+  }
+}
+cudaError_t launch_tridiag_prepare(const double* de, int n, const double* scale,
+                                   double* d, double* e2, double* ae, cudaStream_t st,
+                                   int* launches) {
+  tridiag_prepare_kernel<<<(n + 255) / 256, 256, 0, st>>>(de, n, scale, d, e2, ae);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bisect(const BisectArgs& a, int nsolves_here, int mmax,
                           cudaStream_t st, int* launches) {
   const size_t smem = sizeof(double) * 2 * (size_t)mmax;

@@ -259,8 +259,8 @@ __device__ __forceinline__ void publish(volatile long long* prog, int warp,
   if ((threadIdx.x & 31) == 0) prog[warp] = spos(s, k);
 }
 
-template <int kWarpsPerCta>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, kBulgeCtasPerSm)
+template <int kWarpsPerCta, int kMinBlocks>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, kMinBlocks)
 bulge_chase_kernel(Stage2Args a) {
 #ifdef EIGENID_PHASE_TIMING
   long long t_b_ = clock64();
@@ -426,13 +426,13 @@ extern "C" void eigenid_debug_bulge_cycles(unsigned long long* out) {
 }
 #endif
 
-template <int W>
+template <int W, int B = kBulgeCtasPerSm>
 static cudaError_t launch_chase(const Stage2Args& a, int grid, cudaStream_t st) {
   const size_t smem = sizeof(double) * kWarpSmem * W;
   cudaError_t e = cudaFuncSetAttribute(
-      bulge_chase_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      bulge_chase_kernel<W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  bulge_chase_kernel<W><<<grid, W * 32, smem, st>>>(a);
+  bulge_chase_kernel<W, B><<<grid, W * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -450,6 +450,9 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
     if (w[0] == '8') long_sweeps = false;
     if (w[0] == '9') long_sweeps = true;
   }
+  // lambda(A)'s lone chase beside the narrow stage-1 layout: <= 128
+  // registers so it fits on an SM that still runs a stage-1 CTA
+  if (a.compact) return launch_chase<kWarpsShort, 2>(a, grid, st);
   return long_sweeps ? launch_chase<kWarpsLong>(a, grid, st)
                      : launch_chase<kWarpsShort>(a, grid, st);
 }

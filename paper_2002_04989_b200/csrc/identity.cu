@@ -337,24 +337,45 @@ __global__ void c5_mu_kernel(uint64_t seed, const double* __restrict__ lam,
   }
 }
 
-// evaluate() for one (i, j) with raw value and method (identity.cpp:185-238):
-// checked_min_gap for i (identity.cpp:189), batched product, log-domain
-// retry, clamp.  out3 = {value, raw, method}.
+// One component (i, j), the reference's per-component entry points:
+//   variant 0: evaluate() (identity.cpp:185-238) — checked_min_gap for i
+//              (:189), batched sorted-pairing product with the log-domain
+//              retry, or the log domain outright when cfg is kLogDomain;
+//   variant 2: component_magnitude_baseline (:151-183) — natural pairing,
+//              sequential running products, NonFiniteIntermediate when one
+//              leaves the finite range.
+// out4 = {value, raw, method (EvaluationMethod), condition_flag}.
 __global__ void component_kernel(const double* __restrict__ lam,
                                  const double* __restrict__ mu, int n, int i,
                                  int batch, double tol, int log_domain,
-                                 double* out3, DevStatus* status) {
+                                 int variant, double* out4, DevStatus* status) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double min_gap = 1e308;
+  double min_gap = 1.0 / 0.0;
   for (int k = 0; k < n; ++k)
     if (k != i) min_gap = fmin(min_gap, fabs(lam[i] - lam[k]));
-  if (min_gap <= tol * (lam[n - 1] - lam[0])) {
+  const double range = lam[n - 1] - lam[0];
+  if (min_gap <= tol * range) {
     set_status(status, 2, i, min_gap, -1, 1);
     return;
   }
   double raw;
   int method = 1;
-  if (log_domain) {
+  if (variant == 2) {
+    const double li = lam[i];
+    double num = 1.0, den = 1.0;
+    for (int k = 0; k + 1 < n; ++k) {
+      num = __dmul_rn(num, __dsub_rn(li, mu[k]));
+      if (!isfinite(num)) { set_status(status, 4, i, 0.0, 1); return; }
+    }
+    for (int k = 0; k < n; ++k) {
+      if (k == i) continue;
+      den = __dmul_rn(den, __dsub_rn(li, lam[k]));
+      if (!isfinite(den)) { set_status(status, 4, i, 0.0, 2); return; }
+    }
+    raw = __ddiv_rn(num, den);
+    if (!isfinite(raw)) { set_status(status, 4, i, 0.0, 3); return; }
+    method = 0;
+  } else if (log_domain) {
     const int rc = identity_log_domain(lam, mu, n, i, &raw);
     if (rc) { set_status(status, rc, i, 0.0); return; }
     method = 3;
@@ -366,43 +387,87 @@ __global__ void component_kernel(const double* __restrict__ lam,
       method = 3;
     }
   }
-  out3[0] = clamp01(raw);
-  out3[1] = raw;
-  out3[2] = method;
+  out4[0] = clamp01(raw);
+  out4[1] = raw;
+  out4[2] = method;
+  out4[3] = min_gap / range;
 }
 
-// raw |v_ij|^2 of one eigenvector i for every row j (vector_magnitudes).
+// raw |v_ij|^2 of one eigenvector i for every row j (vector_magnitudes,
+// identity.cpp:276-292) and the method each took (1 batched, 3 log-domain).
 __global__ void vector_kernel(const double* __restrict__ lam,
                               const double* __restrict__ mu, int n, int i,
-                              int batch, double* __restrict__ raw_out,
-                              DevStatus* status) {
+                              int batch, int log_domain, double* __restrict__ raw_out,
+                              double* __restrict__ method_out, DevStatus* status) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += gridDim.x * blockDim.x) {
     const double* mj = mu + (long long)j * (n - 1);
-    double raw = identity_batched(lam, mj, n, i, batch);
-    if (!isfinite(raw)) {
+    double raw = 0.0;
+    int method = 1;
+    if (!log_domain) raw = identity_batched(lam, mj, n, i, batch);
+    if (log_domain || !isfinite(raw)) {
       const int rc = identity_log_domain(lam, mj, n, i, &raw);
       if (rc) set_status(status, rc, i, 0.0, j);
+      method = 3;
     }
     raw_out[j] = raw;
+    if (method_out) method_out[j] = method;
   }
+}
+
+// log_domain_product (identity.cpp:98-122) of explicit factor lists, in list
+// order: out = exp(sum ln|num| - sum ln|den|); a zero numerator gives 0, a
+// zero denominator DegenerateEigenvalue(gap 0), a negative sign
+// InternalInconsistency.
+__global__ void log_product_kernel(const double* __restrict__ num,
+                                   const double* __restrict__ den, long long len,
+                                   double* out, DevStatus* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double log_sum = 0.0;
+  bool negative = false, zero = false;
+  for (long long k = 0; k < len; ++k) {
+    const double x = num[k];
+    if (x == 0.0) {
+      zero = true;
+    } else {
+      log_sum += log(fabs(x));
+      if (x < 0.0) negative = !negative;
+    }
+  }
+  for (long long k = 0; k < len; ++k) {
+    const double x = den[k];
+    if (x == 0.0) { set_status(status, 2, -1, 0.0); return; }
+    log_sum -= log(fabs(x));
+    if (x < 0.0) negative = !negative;
+  }
+  if (zero) { *out = 0.0; return; }
+  if (negative) { set_status(status, 5, -1, 0.0); return; }
+  *out = exp(log_sum);
 }
 
 cudaError_t launch_component(const double* dlam, const double* dmu, int n,
                              int i, int batch, double tol, int log_domain,
-                             double* dout3, DevStatus* dstatus, cudaStream_t st,
-                             int* launches) {
+                             int variant, double* dout4, DevStatus* dstatus,
+                             cudaStream_t st, int* launches) {
   component_kernel<<<1, 32, 0, st>>>(dlam, dmu, n, i, batch, tol, log_domain,
-                                     dout3, dstatus);
+                                     variant, dout4, dstatus);
   ++*launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
-                          int batch, double* draw, DevStatus* dstatus,
-                          cudaStream_t st, int* launches) {
-  vector_kernel<<<(n + 127) / 128, 128, 0, st>>>(dlam, dmu, n, i, batch, draw,
-                                                 dstatus);
+                          int batch, int log_domain, double* draw, double* dmethod,
+                          DevStatus* dstatus, cudaStream_t st, int* launches) {
+  vector_kernel<<<(n + 127) / 128, 128, 0, st>>>(dlam, dmu, n, i, batch, log_domain,
+                                                 draw, dmethod, dstatus);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_log_product(const double* dnum, const double* dden, long long len,
+                               double* dout, DevStatus* dstatus, cudaStream_t st,
+                               int* launches) {
+  log_product_kernel<<<1, 32, 0, st>>>(dnum, dden, len, dout, dstatus);
   ++*launches;
   return cudaGetLastError();
 }

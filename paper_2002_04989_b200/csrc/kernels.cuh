@@ -63,6 +63,7 @@ struct Stage2Args {
   int* counter;            // work queue (zeroed before launch)
   const DevStatus* status; // sticky call status: nonzero code = abort
   int device;              // for the SM count
+  int compact = 0;         // 1: register-capped variant (co-resides with stage 1)
 };
 cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st);
 
@@ -108,11 +109,21 @@ cudaError_t launch_c5_mu(uint64_t seed, const double* dlam, int n, int j0,
                          int rows, double* dmu, cudaStream_t st, int* launches);
 cudaError_t launch_component(const double* dlam, const double* dmu, int n,
                              int i, int batch, double tol, int log_domain,
-                             double* dout3, DevStatus* dstatus, cudaStream_t st,
-                             int* launches);
+                             int variant, double* dout4, DevStatus* dstatus,
+                             cudaStream_t st, int* launches);
 cudaError_t launch_vector(const double* dlam, const double* dmu, int n, int i,
-                          int batch, double* draw, DevStatus* dstatus,
-                          cudaStream_t st, int* launches);
+                          int batch, int log_domain, double* draw, double* dmethod,
+                          DevStatus* dstatus, cudaStream_t st, int* launches);
+cudaError_t launch_log_product(const double* dnum, const double* dden, long long len,
+                               double* dout, DevStatus* dstatus, cudaStream_t st,
+                               int* launches);
+// Tridiagonal helpers (bisect.cu): signed (d, e) of a reduced band, and the
+// (d*s, (e*s)^2, |e*s|) the bisection reads from an explicit tridiagonal.
+cudaError_t launch_band_tridiag(const double* band, int ldab, int n, double* d,
+                                double* e, cudaStream_t st, int* launches);
+cudaError_t launch_tridiag_prepare(const double* de, int n, const double* scale,
+                                   double* d, double* e2, double* ae, cudaStream_t st,
+                                   int* launches);
 
 // ---- recover.cu: sign recovery (signs.cpp:48-120)
 struct RecoverState;

@@ -146,6 +146,56 @@ def c5_lambda(seed: int, n: int) -> np.ndarray:
         lam = np.sort(lam)
 
 
+METHODS = {0: "baseline", 1: "batched", 2: "batched-parallel", 3: "log-domain"}
+
+
+def log_domain_product(numerator, denominator, device: int = 0) -> float:
+    """log_domain_product (identity.cpp:98-122) of explicit factor lists, on
+    the device."""
+    num = np.ascontiguousarray(numerator, np.float64)
+    den = np.ascontiguousarray(denominator, np.float64)
+    if num.size != den.size:
+        raise errors.DimensionMismatch("factor lists differ in length")
+    dev = Device.get(device)
+    out = C.c_double()
+    err = _native.GpuErr()
+    _native.check(dev.lib.eigenid_gpu_log_domain_product(
+        dev.ctx, _native.dptr(num), _native.dptr(den), num.size, C.byref(out),
+        C.byref(err)), err)
+    return out.value
+
+
+def tridiagonalize(a, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """tridiagonalize (eigensolve.hpp:41): (diag, offdiag) of the device
+    reduction — orthogonally similar to A, not tred1's sequence."""
+    n, e = _as_matrix(a)
+    dev = Device.get(device)
+    d = np.empty(n, np.float64)
+    off = np.empty(max(n - 1, 1), np.float64)
+    err = _native.GpuErr()
+    _native.check(dev.lib.eigenid_gpu_tridiagonalize(dev.ctx, _native.dptr(e), n,
+                                                     _native.dptr(d), _native.dptr(off),
+                                                     C.byref(err)), err)
+    return d, off[: n - 1]
+
+
+def tridiagonal_eigenvalues(diag, offdiag, device: int = 0) -> np.ndarray:
+    """eigenvalues(TridiagonalForm) (eigensolve.cpp:72-128) by device Sturm
+    bisection, ascending."""
+    d = np.ascontiguousarray(diag, np.float64)
+    off = np.ascontiguousarray(offdiag, np.float64)
+    n = d.size
+    if n > 0 and off.size != n - 1:
+        raise errors.DimensionMismatch("tridiagonal form needs n-1 off-diagonal values")
+    dev = Device.get(device)
+    out = np.empty(n, np.float64)
+    err = _native.GpuErr()
+    _native.check(dev.lib.eigenid_gpu_tridiagonal_eigenvalues(
+        dev.ctx, _native.dptr(d), _native.dptr(off) if off.size else None, n,
+        _native.dptr(out), C.byref(err)), err)
+    return out
+
+
 def _as_matrix(a) -> tuple[int, np.ndarray]:
     if isinstance(a, SymmetricMatrix):
         return a.n(), np.ascontiguousarray(a.entries())
@@ -176,13 +226,18 @@ class Device:
     _instances: dict[int, "Device"] = {}
     _lock = threading.Lock()
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, num_gpus: int = 1, multi: bool = False):
         self.lib = _native.load()
         self.ctx = C.c_void_p()
         err = _native.GpuErr()
-        _native.check(self.lib.eigenid_gpu_create(C.byref(self.ctx), device,
-                                                  C.byref(err)), err)
+        if num_gpus == 1 and not multi:
+            _native.check(self.lib.eigenid_gpu_create(C.byref(self.ctx), device,
+                                                      C.byref(err)), err)
+        else:  # devices device .. device+num_gpus-1, one NCCL communicator
+            _native.check(self.lib.eigenid_gpu_create_multi(
+                C.byref(self.ctx), device, num_gpus, C.byref(err)), err)
         self.device = device
+        self.num_gpus = num_gpus
 
     @classmethod
     def get(cls, device: int = 0) -> "Device":
@@ -253,13 +308,21 @@ def recover_signs(a, i: int, magnitudes, lambda_i: float, sign_tol: float = 1e-1
 class IdentityEngine:
     """identity.hpp:99-157, the all-magnitudes path on the GPU."""
 
-    def __init__(self, cfg: IdentityConfig | None = None, device: int = 0):
+    def __init__(self, cfg: IdentityConfig | None = None, device: int = 0,
+                 num_gpus: int | None = None):
         self._cfg = cfg or IdentityConfig()
         if self._cfg.batch_size < 1:
             raise errors.ConfigError("batch size must be >= 1")
         if not self._cfg.degeneracy_tol >= 0.0:
             raise errors.ConfigError("degeneracy tolerance must be >= 0")
-        self._dev = Device.get(device)
+        if num_gpus is not None and num_gpus < 1:
+            raise errors.ConfigError("num_gpus must be >= 1")
+        # num_gpus given: an engine-owned multi-device context over devices
+        # device .. device+num_gpus-1 (NCCL communicator, even for one GPU);
+        # all_magnitudes shards the minors and all-gathers rows with NCCL.
+        # None: the process-wide context of `device`.
+        self._dev = Device.get(device) if num_gpus is None else Device(device, num_gpus,
+                                                                         multi=True)
         self._solves = 0
         self._solves_lock = threading.Lock()
 
@@ -358,6 +421,50 @@ class IdentityEngine:
         self._count(b)
         _native.check(st, err)
         return v.value, r.value, m.value
+
+    def _component(self, a, i, j, cached_lambda, cached_mu, variant) -> dict:
+        n, e = _as_matrix(a)
+        lam = None if cached_lambda is None else np.ascontiguousarray(cached_lambda, np.float64)
+        mu = None if cached_mu is None else np.ascontiguousarray(cached_mu, np.float64)
+        m = _native.GpuMagnitude()
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        b = self._before()
+        st = self._dev.lib.eigenid_gpu_component(
+            self._dev.ctx, _native.dptr(e), n, i, j,
+            _native.dptr(lam) if lam is not None else None,
+            _native.dptr(mu) if mu is not None else None, C.byref(cfg), variant,
+            C.byref(m), C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        return {"value": m.value, "raw_value": m.raw_value, "i": i, "j": j,
+                "method": METHODS[m.method], "condition_flag": m.condition_flag}
+
+    def component_magnitude_baseline(self, a, i: int, j: int) -> dict:
+        """MagnitudeResult of component_magnitude_baseline (identity.cpp:151-183):
+        natural pairing, sequential running products on the device, 2 solves;
+        NonFiniteIntermediate when a product leaves the finite range."""
+        return self._component(a, i, j, None, None, 2)
+
+    def component_result(self, a, i: int, j: int, cached_lambda=None,
+                         cached_mu=None) -> dict:
+        """Full MagnitudeResult of component_magnitude (identity.cpp:240-251)."""
+        return self._component(a, i, j, cached_lambda, cached_mu, 0)
+
+    def vector_results(self, a, i: int) -> list[dict]:
+        """vector_magnitudes (identity.cpp:276-292) as MagnitudeResult dicts."""
+        n, e = _as_matrix(a)
+        out = (_native.GpuMagnitude * n)()
+        err = _native.GpuErr()
+        cfg = self._cfg._c()
+        b = self._before()
+        st = self._dev.lib.eigenid_gpu_vector(self._dev.ctx, _native.dptr(e), n, i,
+                                              C.byref(cfg), out, C.byref(err))
+        self._count(b)
+        _native.check(st, err)
+        return [{"value": m.value, "raw_value": m.raw_value, "i": i, "j": j,
+                 "method": METHODS[m.method], "condition_flag": m.condition_flag}
+                for j, m in enumerate(out)]
 
     def log_domain_magnitude(self, a, i: int, j: int, cached_lambda=None,
                              cached_mu=None):

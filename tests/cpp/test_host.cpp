@@ -5,8 +5,12 @@
 #include <cstdio>
 #include <vector>
 
+#include <cstring>
+
 #include "eigenid/errors.hpp"
 #include "eigenid/identity.hpp"
+#include "eigenid/matrix_io.hpp"
+#include "eigenid_b200.h"
 
 using namespace eigenid;
 
@@ -88,6 +92,81 @@ int main() {
     try { recover_signs(m, 0, junk, 123.0); } catch (const SignRecoveryFailure&) { a = true; }
     try { recover_signs(m, 0, std::vector<double>(9, 0.1), 123.0); } catch (const DimensionMismatch&) { b = true; }
     report("recover-signs-errors", a && b);
+  }
+  {  // the rest of the reference surface: matrix / spectrum helpers
+    auto a = random_symmetric(7, 30);
+    double tr = 0.0, fro = 0.0;
+    for (std::size_t i = 0; i < 30; ++i) tr += a(i, i);
+    for (double v : a.entries()) fro += v * v;
+    auto s = eigenvalues(a);
+    report("trace-frobenius-sum", a.trace() == tr && a.frobenius_norm() == std::sqrt(fro) &&
+                                      std::fabs(s.sum() - tr) <= 1e-12);
+    // tridiagonalize + eigenvalues(TridiagonalForm) reproduce eigenvalues(A)
+    auto t = tridiagonalize(a);
+    auto st = eigenvalues(t);
+    double dev = 0.0;
+    for (std::size_t i = 0; i < 30; ++i) dev = std::fmax(dev, std::fabs(st[i] - s[i]));
+    report("tridiagonal-form", t.diag.size() == 30 && t.offdiag.size() == 29 && dev <= 1e-12);
+  }
+  {  // per-component entries agree with all_magnitudes (acceptance.cpp:130-174)
+    auto a = random_symmetric(3000, 24);
+    auto all = engine.all_magnitudes(a);
+    IdentityEngine base;
+    base.reset_solve_count();
+    auto rb = base.component_magnitude_baseline(a, 5, 7);
+    auto rc = base.component_magnitude(a, 5, 7);
+    auto rl = base.log_domain_magnitude(a, 5, 7);
+    const double want = all[7 * 24 + 5];
+    bool ok = std::fabs(rb.value - want) <= 1e-10 * want && std::fabs(rc.value - want) <= 1e-12 &&
+              std::fabs(rl.value - want) <= 1e-10 * want;
+    ok = ok && rb.method == EvaluationMethod::kBaseline &&
+         rl.method == EvaluationMethod::kLogDomain && rb.i == 5 && rb.j == 7 &&
+         rc.condition_flag > 0.0 && base.eigenvalue_solve_count() == 6;
+    report("component-variants", ok);
+    auto v = base.vector_magnitudes(a, 5);
+    double vdev = 0.0, vs = 0.0;
+    for (std::size_t j = 0; j < 24; ++j) {
+      vdev = std::fmax(vdev, std::fabs(v[j].value - all[j * 24 + 5]));
+      vs += v[j].value;
+    }
+    report("vector-magnitudes", v.size() == 24 && vdev <= 1e-12 && std::fabs(vs - 1) <= 1e-10);
+    // pairing / batches / log-domain product helpers (identity.cpp:59-122)
+    auto sa = eigenvalues(a), sm = eigenvalues(a.minor_matrix(7));
+    auto f = make_sorted_pairing(sa, sm, 5);
+    auto plan = prepare_batches(f, 8);
+    const double lp = log_domain_product(f);
+    report("pairing-helpers", f.size() == 23 && plan.batch_count() == 3 &&
+                                  plan.batches[2].size() == 7 &&
+                                  std::fabs(lp - rl.raw_value) <= 1e-13 * lp);
+    bool nf = false, deg = false;
+    try {  // the naive products overflow at n = 300, x1e3 (acceptance.cpp:198-231)
+      auto big = random_symmetric(1, 300).scaled(1e3);
+      for (std::size_t i = 0; i < 300 && !nf; i += 37)
+        for (std::size_t j = 0; j < 300 && !nf; j += 53) base.component_magnitude_baseline(big, i, j);
+    } catch (const NonFiniteIntermediate&) { nf = true; }
+    try { base.component_magnitude_baseline(SymmetricMatrix::identity(5), 0, 0); }
+    catch (const DegenerateEigenvalue&) { deg = true; }
+    report("baseline-errors", nf && deg);
+  }
+  {  // multi-device context over the visible GPUs: bit-identical to one GPU
+    int ndev = eigenid_gpu_device_count();
+    eigenid_gpu_ctx* multi = nullptr;
+    eigenid_gpu_err e{};
+    const int st = eigenid_gpu_create_multi(&multi, 0, ndev < 8 ? ndev : 8, &e);
+    bool ok = st == EIGENID_OK;
+    if (ok) {
+      auto a = random_symmetric(11, 200).scaled(0.1);
+      auto want = engine.all_magnitudes(a);
+      std::vector<double> got(200 * 200);
+      eigenid_gpu_config c{64, 1e-12, 0};
+      ok = eigenid_gpu_all_magnitudes(multi, a.entries().data(), 200, &c, got.data(), nullptr,
+                                      nullptr, &e) == EIGENID_OK &&
+           std::memcmp(got.data(), want.data(), sizeof(double) * got.size()) == 0;
+      eigenid_gpu_destroy(multi);
+    } else {
+      std::printf("create_multi: %s\n", e.msg);
+    }
+    report("multi-gpu-nccl", ok);
   }
   return failures;
 }

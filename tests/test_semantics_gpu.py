@@ -110,7 +110,8 @@ def test_extreme_input_scales(engine, oracle, n, s):
     g, lam, _ = engine.all_magnitudes(a, return_spectra=True)
     g = g.reshape(n, n)
     c, lc, _ = oracle.all_magnitudes(a, return_spectra=True)
-    c0 = oracle.all_magnitudes(a0).reshape(n, n)
+    c0, lc0, _ = oracle.all_magnitudes(a0, return_spectra=True)
+    c0 = c0.reshape(n, n)
     assert np.all(np.isfinite(g))
     # the reference's own results move with the scale (row scaling by
     # sum|a| rounds; near 1e-300 its QL meets subnormals): the GPU must agree
@@ -118,7 +119,10 @@ def test_extreme_input_scales(engine, oracle, n, s):
     spread = float(np.max(np.abs(c.reshape(n, n) - c0)))
     assert mixed_ok(g, c.reshape(n, n), abs_=1e-11 + spread)
     assert mixed_ok(g, c0, abs_=1e-11)
-    assert np.max(np.abs(lam - lc)) <= 1e-12 * np.max(np.abs(lc))
+    # eigenvalues: against the unscaled problem's, scaled back (the
+    # reference's own near 1e-300 drift into subnormals)
+    want = lc0 * s
+    assert np.max(np.abs(lam - want)) <= 1e-12 * np.max(np.abs(want))
 
 
 @pytest.mark.parametrize("n", [10, 100])
@@ -201,3 +205,92 @@ def test_degenerate_lambda_stops_before_the_minor_solves(engine):
     t_deg = time.perf_counter() - t
     assert engine.eigenvalue_solve_count() == 1
     assert t_deg < 0.5 * t_good, (t_deg, t_good)
+
+
+def test_reference_acceptance_suite_against_the_dropin():
+    """The reference's own acceptance suite (proj/tests/acceptance.cpp,
+    compiled unmodified against include/eigenid/*.hpp + libeigenid.so, with
+    the reference's Jacobi oracle from oracle/_ref): all nine criteria that do
+    not time the CPU bench harness pass on the device."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("acceptance binary not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, "--skip-performance"], capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    passed = [ln for ln in r.stdout.splitlines() if ln.startswith("[PASS]")]
+    assert len(passed) == 9, r.stdout
+
+
+def test_component_variants_and_results(engine, oracle):
+    """component_magnitude_baseline / component_magnitude / log_domain_magnitude
+    / vector_magnitudes with full MagnitudeResult fields (identity.hpp:66-74)."""
+    import paper_2002_04989_b200 as eid
+    from paper_2002_04989_b200.engine import log_domain_product
+    a = oracle.random_symmetric(3001, 40)
+    all_ = engine.all_magnitudes(a).reshape(40, 40)
+    c, lam, mu = oracle.all_magnitudes(a, return_spectra=True)
+    rb = engine.component_magnitude_baseline(a, 4, 9)
+    rc = engine.component_result(a, 4, 9)
+    assert rb["method"] == "baseline" and rc["method"] == "batched"
+    assert abs(rb["value"] - all_[9, 4]) <= 1e-10 * all_[9, 4]
+    gaps = np.abs(lam[4] - np.delete(lam, 4))
+    assert abs(rc["condition_flag"] - gaps.min() / (lam[-1] - lam[0])) <= 1e-12
+    # cached spectra: bit-exact with the oracle's evaluate()
+    r = engine.component_result(a, 4, 9, lam, mu[9])
+    assert (r["value"], r["raw_value"]) == oracle.evaluate(lam, mu[9], 4)[:2]
+    vr = engine.vector_results(a, 4)
+    assert [x["j"] for x in vr] == list(range(40))
+    assert max(abs(x["value"] - all_[j, 4]) for j, x in enumerate(vr)) <= 1e-12
+    # log_domain_product of explicit factor lists (sorted pairing)
+    num = np.sort(lam[4] - mu[9])
+    den = np.sort(lam[4] - np.delete(lam, 4))
+    lp = log_domain_product(num, den)
+    assert abs(lp - oracle.log_domain_product(num, den)) <= 1e-13 * lp
+    with pytest.raises(eid.DegenerateEigenvalue):
+        log_domain_product([1.0, 2.0], [0.0, 1.0])
+    with pytest.raises(eid.InternalInconsistency):
+        log_domain_product([1.0, -2.0], [1.0, 1.0])
+    with pytest.raises(eid.NonFiniteIntermediate):  # acceptance.cpp:198-231's probe
+        big = oracle.random_symmetric(1, 300) * 1e3
+        for i in range(0, 300, 37):
+            for j in range(0, 300, 53):
+                engine.component_magnitude_baseline(big, i, j)
+
+
+def test_tridiagonal_entries(oracle):
+    """tridiagonalize / eigenvalues(TridiagonalForm) (eigensolve.hpp:41-47):
+    the device tridiagonal is orthogonally similar to A (same spectrum,
+    trace, Frobenius norm) and its bisection reproduces the oracle's QL."""
+    from paper_2002_04989_b200.engine import tridiagonal_eigenvalues, tridiagonalize
+    for n in (2, 17, 100, 300):
+        a = oracle.random_symmetric(40 + n, n)
+        d, e = tridiagonalize(a)
+        assert abs(d.sum() - np.trace(a)) <= 1e-11 * n
+        assert abs(np.sum(d * d) + 2 * np.sum(e * e) - np.sum(a * a)) <= 1e-10 * np.sum(a * a)
+        lam = tridiagonal_eigenvalues(d, e)
+        assert np.max(np.abs(lam - oracle.eigenvalues(a))) <= 1e-13 * n
+        # and the reference's own tridiagonal through the device bisection
+        dr, er = oracle.tridiagonalize(a)
+        assert np.max(np.abs(tridiagonal_eigenvalues(dr, er) - oracle.ql(dr, er))) <= 1e-13 * n
+
+
+def test_multi_gpu_context_bit_identical(oracle):
+    """A multi-device context (ncclCommInitAll over every visible GPU; on a
+    one-GPU box a communicator of one) shards the minors over the devices and
+    all-gathers the rows with NCCL inside all_magnitudes: bit-identical to
+    the single-device engine, n+1 solves."""
+    import torch
+
+    from paper_2002_04989_b200 import IdentityEngine
+    ndev = min(torch.cuda.device_count(), 8)
+    multi = IdentityEngine(num_gpus=ndev)
+    single = IdentityEngine()
+    for n in (48, 257):  # fused small path and the two-stage path
+        a = oracle.random_symmetric(70 + n, n)
+        multi.reset_solve_count()
+        g = multi.all_magnitudes(a)
+        assert multi.eigenvalue_solve_count() == n + 1
+        assert np.array_equal(bits(g), bits(single.all_magnitudes(a)))
