@@ -69,6 +69,10 @@ constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
 #ifndef EIGENID_STAGE1_FUSED
 #define EIGENID_STAGE1_FUSED 1
 #endif
+// split arrive / sync around the fused tile's row product (see gemm_fused)
+#ifndef EIGENID_SPLIT_BAR
+#define EIGENID_SPLIT_BAR 0
+#endif
 // Fused pass (rest of panel p's update + SYMM of panel p+1): kFS stages of
 // {Bop rows, C tile, VT(cb) rows} plus the row block's VT(rb) rows.
 constexpr int kFVLD = 34, kFVRLD = 36;
@@ -943,6 +947,17 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
       }
+#if EIGENID_SPLIT_BAR
+      // updated C rows to shared memory first, then arrive (non-blocking) on
+      // the "C tile complete" barrier, and run this warp's independent row
+      // product while the other warps arrive: the DMMA pipe is fed across
+      // the barrier instead of draining at it
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt)
+        *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
+            make_double2(acc[nt][0], acc[nt][1]);
+      asm volatile("bar.arrive 1, %0;\n" ::"n"(kNT) : "memory");
+#endif
       // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators: the
       // m8n8k4 accumulator of column tile q holds C[row][8q+2kk .. +1], which
       // is exactly this lane's A-fragment pair for k-pair q (no shared-memory
@@ -977,11 +992,15 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         }
       };
       store_c();
+#if EIGENID_SPLIT_BAR
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kNT) : "memory");
+#else
 #pragma unroll
       for (int nt = 0; nt < kG2N / 8; ++nt)
         *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
             make_double2(acc[nt][0], acc[nt][1]);
       __syncthreads();
+#endif
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 8*kXT cols)
       {
         const int ccol = 8 * mt2 + mm;  // tile column of C = X row
