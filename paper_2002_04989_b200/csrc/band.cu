@@ -71,7 +71,7 @@ constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
 #endif
 // split arrive / sync around the fused tile's row product (see gemm_fused)
 #ifndef EIGENID_SPLIT_BAR
-#define EIGENID_SPLIT_BAR 0
+#define EIGENID_SPLIT_BAR 1
 #endif
 // Fused pass (rest of panel p's update + SYMM of panel p+1): kFS stages of
 // {Bop rows, C tile, VT(cb) rows} plus the row block's VT(rb) rows.
