@@ -832,6 +832,32 @@ __device__ __forceinline__ int cswz(int row, int col) {
   return row * kG2N + (col ^ ((8 * (row & 1)) ^ (4 * ((row >> 1) & 1))));
 }
 
+// mbarrier helpers (CTA scope): arrive has release, try_wait acquire
+// semantics, so shared-memory writes before an arrival are visible to a
+// thread whose wait on that phase has returned.
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+}
+
 __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                            const double* Vp, const double* VTn, double* Xn,
                            double* sm) {
@@ -839,6 +865,15 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
   const int kk = lane & 3, mm = lane >> 2;
   const int crow = 8 * warp + mm;
   double* sVr = sm + kFS * kFSt;
+#if EIGENID_SPLIT_BAR
+  // "every warp's updated C rows are in shared memory": one arrival per warp
+  // per tile, phases alternate tile by tile
+  __shared__ alignas(8) unsigned long long cbar_storage;
+  unsigned long long* cbar = &cbar_storage;
+  unsigned cphase = 0;
+  if (tid == 0) mbar_init(cbar, kNW);
+  __syncthreads();
+#endif
   for (int rb = 0; rb < sn; rb += kG2M) {
     const int r = rb + crow;
     double2 af[kG2K / 8];
@@ -949,14 +984,15 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       }
 #if EIGENID_SPLIT_BAR
       // updated C rows to shared memory first, then arrive (non-blocking) on
-      // the "C tile complete" barrier, and run this warp's independent row
-      // product while the other warps arrive: the DMMA pipe is fed across
-      // the barrier instead of draining at it
+      // the "C tile complete" mbarrier (one arrival per warp), and run this
+      // warp's independent row product before waiting for the others: the
+      // DMMA pipe is fed across the barrier instead of draining at it
 #pragma unroll
       for (int nt = 0; nt < kG2N / 8; ++nt)
         *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
             make_double2(acc[nt][0], acc[nt][1]);
-      asm volatile("bar.arrive 1, %0;\n" ::"n"(kNT) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cbar);
 #endif
       // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators: the
       // m8n8k4 accumulator of column tile q holds C[row][8q+2kk .. +1], which
@@ -993,7 +1029,8 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       };
       store_c();
 #if EIGENID_SPLIT_BAR
-      asm volatile("bar.sync 1, %0;\n" ::"n"(kNT) : "memory");
+      mbar_wait(cbar, cphase);
+      cphase ^= 1u;
 #else
 #pragma unroll
       for (int nt = 0; nt < kG2N / 8; ++nt)

@@ -452,7 +452,9 @@ cudaError_t launch_stage2(const Stage2Args& a, cudaStream_t st) {
   }
   // lambda(A)'s lone chase beside the narrow stage-1 layout: <= 128
   // registers so it fits on an SM that still runs a stage-1 CTA
-  if (a.compact) return launch_chase<kWarpsShort, 2>(a, grid, st);
+  bool compact = a.compact;
+  if (const char* c = std::getenv("EIGENID_STAGE2_COMPACT")) compact = compact || c[0] == '1';
+  if (compact) return launch_chase<kWarpsShort, 2>(a, grid, st);
   return long_sweeps ? launch_chase<kWarpsLong>(a, grid, st)
                      : launch_chase<kWarpsShort>(a, grid, st);
 }

@@ -294,3 +294,19 @@ def test_multi_gpu_context_bit_identical(oracle):
         g = multi.all_magnitudes(a)
         assert multi.eigenvalue_solve_count() == n + 1
         assert np.array_equal(bits(g), bits(single.all_magnitudes(a)))
+
+
+@pytest.mark.parametrize("n,rows", [(1024, 1024), (2000, 400), (3100, 300)])
+def test_repeat_runs_are_bit_identical(engine, n, rows):
+    """The reference's determinism contract (bit-identical across worker
+    counts, test_identity.cpp:130-143) on the device: repeated calls give the
+    same bits whatever the solve -> CTA / workspace-slot assignment of the
+    work queues, in both stage-1 layouts (narrow below n = 3072, wide
+    above) and with lambda(A) on the side stream."""
+    import paper_2002_04989_b200 as eid
+    a = eid.random_symmetric(7, n) * np.sqrt(2.0 / n)
+    ref = engine.minor_spectra(a, 0, rows)
+    for _ in range(2):
+        got = engine.minor_spectra(a, 0, rows)
+        assert np.array_equal(bits(got[0]), bits(ref[0]))
+        assert np.array_equal(bits(got[1]), bits(ref[1]))
