@@ -81,9 +81,9 @@ def f_id(n: int, rows: int) -> float:
 
 
 def f_chase(n: int, rows: int, b: int = 32) -> float:
-    """Bulge chase, ~6 b m^2 flops per solve (one Householder of length b per
-    step applied two-sided to a (b+1)-wide band window, m^2/b steps... per
-    DESIGN §4)."""
+    """Bulge chase, ~6 b m^2 flops per solve: m^2 / (2b) chase steps, each a
+    length-b reflector applied from the right and left to a b x b block and
+    two-sided to a b x b diagonal block (~12 b^2 flops)."""
     return 6.0 * b * (n ** 2 + rows * (n - 1) ** 2)
 
 
@@ -646,10 +646,10 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
         t1 = st["stage1"] / 1e3
         achieved = f_tri(n, rows) / t1 / 1e12
         # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
-        # --set full capture (profiles/r01h_band_4096_wide_raw_summary.csv:
-        # 2.053 TB read + 1.231 TB written over 296 solves), scaled to this
+        # --set full capture (profiles/r02a_band_4096_wide_raw_summary.csv:
+        # 1.0106 TB read + 0.6102 TB written over 147 solves), scaled to this
         # launch's solve count
-        traffic = (2.052512e12 + 1.230878e12) / 296 * (rows + 1) if n == 4096 else None
+        traffic = (1.010597e12 + 0.610218e12) / 147 * (rows + 1) if n == 4096 else None
         line["roofline"] = {
             "bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
             "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",

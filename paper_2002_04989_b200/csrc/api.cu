@@ -411,6 +411,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
     solve_list_kernel<<<(cnt0 + 255) / 256, 256, 0, st>>>(djs, j0, 0, cnt0);
     ++launches;
     EID_CUDA(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st), "counter");
+    EID_CUDA(cudaMemsetAsync(ctr + 4, 0, sizeof(int), st), "running flag");
   }
   EID_CUDA(c->bScale.ensure(sizeof(double) * 4), "alloc scale");
   double* dscale = c->bScale.as<double>();
@@ -425,7 +426,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   EID_CUDA(cudaEventRecord(c->ev_a0, sa), "event");
   Stage1Args s1a{dA, n, djsA, 1, c->bWs.as<double>(), ws_stride, ldw,
                  c->bBandA.as<double>(), band_stride, ctr + 2, c->dstatus, slot_a,
-                 dscale};
+                 dscale, nullptr, 0};
   EID_CUDA(launch1(s1a, 1, sa, true), "stage1 A");
   Stage2Args s2a{c->bBandA.as<double>(), band_stride, djsA, 1, n, dA_d, dA_d + n,
                  dA_d + 2 * n, n, ctr + 3, c->dstatus, c->device, cps > 1 ? 1 : 0};
@@ -439,11 +440,13 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
              "degeneracy");
   EID_CUDA(cudaEventRecord(c->ev_a1, sa), "event");  // lambda(A) + degeneracy done
   Stage1Args s1{dA, n, djs, cnt0, c->bWs.as<double>(), ws_stride, ldw,
-                c->bBand.as<double>(), band_stride, ctr + 1, c->dstatus, 0, dscale};
+                c->bBand.as<double>(), band_stride, ctr + 1, c->dstatus, 0, dscale,
+                ctr + 4, 0};
   const int grid_main = side_ok ? (cnt0 < slot_a ? cnt0 : slot_a) : (cnt0 < slots ? cnt0 : slots);
   if (side_ok && cnt0 > grid_main) {
     Stage1Args h = s1;
     h.slot0 = slot_a;
+    h.helper = 1;
     const int hg = cnt0 - grid_main < cps ? cnt0 - grid_main : cps;
     EID_CUDA(launch1(h, hg, sa, false), "stage1 helper");
     ++launches;
@@ -461,6 +464,7 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
       solve_list_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(djs, j0, (int)g0, cnt);
       ++launches;
       s1.nsolves = cnt;
+      s1.running = nullptr;  // no helper for the later chunks
       EID_CUDA(launch1(s1, cnt < slots ? cnt : slots, st, true), "stage1");
     }
     ++launches;

@@ -1154,6 +1154,13 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
   // progress at the same rate, so a static blockIdx stride leaves one of
   // them running alone at the end of every wave.
   __shared__ int s_sidx;
+  if (args.running) {
+    if (!args.helper) {
+      if (blockIdx.x == 0 && tid == 0) atomicExch(args.running, 1);
+    } else if (*(volatile int*)args.running == 0) {
+      return;  // the main grid is not running beside us (serialised launches)
+    }
+  }
   for (;;) {
     // a failed call (non-finite input, degenerate lambda(A)) stops pulling
     if (tid == 0)

@@ -32,6 +32,12 @@ struct Stage1Args {
   const DevStatus* status;  // sticky call status: nonzero code = abort
   int slot0;          // workspace slot of blockIdx.x == 0
   const double* scale;  // [0]: exact power-of-two input scale (nullable = 1)
+  // "the main grid is running" flag (nullable): the main launch sets it, a
+  // helper launch joins the queue only if it is set — when kernels are
+  // serialised (ncu, CUDA_LAUNCH_BLOCKING) the one-CTA helper would
+  // otherwise drain the whole queue alone before the main grid starts
+  int* running;
+  int helper;         // 1: this launch is the helper
 };
 // Two compiled layouts of the same kernel (band.cu header): wide (16 warps,
 // one CTA per SM) and narrow (8 warps, two CTAs per SM).
