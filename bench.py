@@ -623,6 +623,7 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
     else:
         if world == 1:
             mu_host = mu_dev.cpu().numpy()
+            eng.identity(lam_host, mu_host)   # untimed: one-time pinned staging buffers
             t = time.perf_counter()
             for _ in range(e2e_steps):
                 res = eng.identity(lam_host, mu_host)

@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types only: NCCL is loaded on demand (see NcclApi)
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <random>
@@ -92,6 +93,28 @@ struct DevBuf {
   }
 };
 
+// Pinned host staging buffer, grown on demand and kept by the context.
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
 }  // namespace
 
 struct eigenid_gpu_ctx {
@@ -116,6 +139,8 @@ struct eigenid_gpu_ctx {
   // single-device context per further GPU, one NCCL communicator per GPU
   int ngpu = 1;
   bool multi = false;  // created by eigenid_gpu_create_multi (NCCL path, any P)
+  HostBuf hIn, hOut;   // pinned staging of the streamed host-pointer identity
+  cudaEvent_t ev_io[4] = {};
   eigenid_gpu_ctx* peer[8] = {};
   ncclComm_t comm[8] = {};
 };
@@ -936,6 +961,10 @@ int eigenid_gpu_destroy(eigenid_gpu_ctx* c) {
     b->release();
   cudaFree(c->dstatus);
   cudaFreeHost(c->hstatus);
+  c->hIn.release();
+  c->hOut.release();
+  for (cudaEvent_t& ev : c->ev_io)
+    if (ev) cudaEventDestroy(ev);
   cudaEventDestroy(c->ev_start);
   cudaEventDestroy(c->ev_a);
   cudaEventDestroy(c->ev_a0);
@@ -1150,6 +1179,71 @@ int eigenid_gpu_minor_spectra(eigenid_gpu_ctx* c, const double* a, size_t n,
   return st;
 }
 
+}  // extern "C"
+
+namespace {
+// Host-pointer identity stage for inputs larger than one staging chunk
+// (C5: 8.6 GB of mu in, 8.6 GB of |v|^2 out): rows stream through two pinned
+// buffers each way, so the host copies of chunk c+1 / c-1 and the transfers
+// overlap the identity kernel of chunk c.  Every row is computed by the same
+// kernel whatever the chunking, so the bits are those of the one-shot path.
+int identity_streamed(eigenid_gpu_ctx* c, const double* lambda, const double* mu,
+                      size_t n, size_t rows, size_t chunk,
+                      const eigenid_gpu_config* cfg, double* out, eigenid_gpu_err* err) {
+  const size_t nch = (rows + chunk - 1) / chunk;
+  const size_t in_row = n - 1, out_row = n;
+  EID_CUDA(c->hIn.ensure(sizeof(double) * 2 * chunk * in_row), "pinned in");
+  EID_CUDA(c->hOut.ensure(sizeof(double) * 2 * chunk * out_row), "pinned out");
+  EID_CUDA(c->bMu.ensure(sizeof(double) * 2 * chunk * in_row), "alloc mu");
+  EID_CUDA(c->bOut.ensure(sizeof(double) * 2 * chunk * out_row), "alloc out");
+  for (cudaEvent_t& ev : c->ev_io)
+    if (!ev) EID_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  int launches = 0;
+  EID_CUDA(launch_degeneracy(c->bLam.as<double>(), (int)n, cfg->degeneracy_tol, c->dstatus,
+                             c->stream, &launches), "degeneracy");
+  const int batch = batch_of(cfg, (int)n);
+  const int nb = identity_nb((int)n, batch);
+  EID_CUDA(c->bDen.ensure(sizeof(double) * n * nb), "alloc den");
+  EID_CUDA(c->bRcp.ensure(sizeof(double) * n * nb), "alloc rcp");
+  const long long cap = 1 << 20;
+  EID_CUDA(c->bFlags.ensure(sizeof(long long) * cap), "alloc flags");
+  EID_CUDA(c->bFlagCount.ensure(sizeof(unsigned long long)), "alloc flagc");
+  auto rows_of = [&](size_t k) { return std::min(chunk, rows - k * chunk); };
+  for (size_t k = 0; k <= nch; ++k) {
+    if (k < nch) {
+      const int s = (int)(k & 1);
+      double* hin = c->hIn.as<double>() + s * chunk * in_row;
+      if (k >= 2) EID_CUDA(cudaEventSynchronize(c->ev_io[s]), "in slot");
+      std::memcpy(hin, mu + k * chunk * in_row, sizeof(double) * rows_of(k) * in_row);
+      double* dmu = c->bMu.as<double>() + s * chunk * in_row;
+      double* dout = c->bOut.as<double>() + s * chunk * out_row;
+      EID_CUDA(cudaMemcpyAsync(dmu, hin, sizeof(double) * rows_of(k) * in_row,
+                               cudaMemcpyHostToDevice, c->stream), "H2D mu");
+      EID_CUDA(cudaEventRecord(c->ev_io[s], c->stream), "event");
+      EID_CUDA(launch_identity(c->bLam.as<double>(), dmu, (int)n, (int)rows_of(k), batch,
+                               c->bDen.as<double>(), c->bRcp.as<double>(), dout,
+                               c->bFlagCount.as<unsigned long long>(),
+                               c->bFlags.as<long long>(), cap, c->dstatus, cfg->log_domain,
+                               c->stream, &launches), "identity");
+      EID_CUDA(cudaMemcpyAsync(c->hOut.as<double>() + s * chunk * out_row, dout,
+                               sizeof(double) * rows_of(k) * out_row, cudaMemcpyDeviceToHost,
+                               c->stream), "D2H out");
+      EID_CUDA(cudaEventRecord(c->ev_io[2 + s], c->stream), "event");
+    }
+    if (k >= 1) {  // chunk k-1's rows, while the device works on chunk k
+      const int s = (int)((k - 1) & 1);
+      EID_CUDA(cudaEventSynchronize(c->ev_io[2 + s]), "out slot");
+      std::memcpy(out + (k - 1) * chunk * out_row, c->hOut.as<double>() + s * chunk * out_row,
+                  sizeof(double) * rows_of(k - 1) * out_row);
+    }
+  }
+  c->launches += launches;
+  return EIGENID_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int eigenid_gpu_identity(eigenid_gpu_ctx* c, const double* lambda,
                          const double* mu, size_t n, size_t j0, size_t j1,
                          const eigenid_gpu_config* cfg, double* out,
@@ -1166,6 +1260,15 @@ int eigenid_gpu_identity(eigenid_gpu_ctx* c, const double* lambda,
   std::lock_guard<std::mutex> g(c->mu);
   if ((st = begin(c, err))) return st;
   EID_CUDA(c->bLam.ensure(sizeof(double) * n), "alloc lam");
+  // more than ~4 chunks of 256 MB of output: stream the rows
+  size_t chunk = ((size_t)(256u << 20) / (sizeof(double) * n)) & ~(size_t)31;
+  if (chunk < 32) chunk = 32;
+  if (!cfg->log_domain && rows >= 4 * chunk) {
+    EID_CUDA(cudaMemcpyAsync(c->bLam.p, lambda, sizeof(double) * n, cudaMemcpyHostToDevice,
+                             c->stream), "H2D lambda");
+    if ((st = identity_streamed(c, lambda, mu, n, rows, chunk, cfg, out, err))) return st;
+    return finish(c, err, nullptr);
+  }
   EID_CUDA(c->bMu.ensure(sizeof(double) * rows * (n - 1)), "alloc mu");
   EID_CUDA(c->bOut.ensure(sizeof(double) * rows * n), "alloc out");
   EID_CUDA(cudaMemcpyAsync(c->bLam.p, lambda, sizeof(double) * n,

@@ -310,3 +310,30 @@ def test_repeat_runs_are_bit_identical(engine, n, rows):
         got = engine.minor_spectra(a, 0, rows)
         assert np.array_equal(bits(got[0]), bits(ref[0]))
         assert np.array_equal(bits(got[1]), bits(ref[1]))
+
+
+def test_streamed_host_identity_matches_device_path(oracle):
+    """The host-pointer identity stage streams large inputs through pinned
+    staging buffers chunk by chunk (n = 12288: 12 chunks of 1024 rows); the
+    rows must equal the one-shot device-pointer path bit for bit, and the
+    reference semantics on sampled rows."""
+    import torch
+
+    from paper_2002_04989_b200 import IdentityEngine
+    n = 12288
+    eng = IdentityEngine()
+    lam = oracle.c5_lambda(9, n)
+    lam_d = torch.from_numpy(lam).cuda()
+    mu_d = torch.empty((n, n - 1), dtype=torch.float64, device="cuda")
+    eng.c5_mu_device(9, lam_d.data_ptr(), n, 0, n, mu_d.data_ptr())
+    out_d = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    eng.identity_device(lam_d.data_ptr(), mu_d.data_ptr(), n, 0, n, out_d.data_ptr())
+    eng.sync()
+    mu = mu_d.cpu().numpy()
+    del mu_d
+    want = out_d.cpu().numpy()
+    del out_d
+    got = eng.identity(lam, mu)
+    assert np.array_equal(bits(got), bits(want))
+    rows = [0, 1023, 1024, 6000, n - 1]
+    assert np.array_equal(bits(got[rows]), bits(oracle.identity_rows(lam, mu[rows])))
