@@ -1029,7 +1029,9 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       };
       store_c();
 #if EIGENID_SPLIT_BAR
+#ifndef EIGENID_EXP_NO_CBAR
       mbar_wait(cbar, cphase);
+#endif
       cphase ^= 1u;
 #else
 #pragma unroll
@@ -1039,6 +1041,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       __syncthreads();
 #endif
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 8*kXT cols)
+#ifndef EIGENID_EXP_NO_XT
       {
         const int ccol = 8 * mt2 + mm;  // tile column of C = X row
 #pragma unroll 4
@@ -1057,10 +1060,13 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                 make_double2(x2[u][0], x2[u][1]);
         }
       }
+#endif
     };
     for (int ci = 0; ci < ncb; ++ci) {
       cpa_wait<kFS - 2>();
+#ifndef EIGENID_EXP_NO_TILE_SYNC
       __syncthreads();
+#endif
       stage(ci + kFS - 1);
       if (ci * kG2N + kB > rb)
         tile(ci, std::true_type{});
