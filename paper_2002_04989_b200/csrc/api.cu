@@ -311,6 +311,10 @@ int nccl_fail(eigenid_gpu_err* err, ncclResult_t r, const char* where) {
 // Same-box A/B: the wide stage-1 layout wins at n = 4096, the
 // narrow one at n = 1024.
 constexpr int kStage1WideMinN = 3072;
+#ifndef EIGENID_STAGE1_LARGE_LAYOUT
+#define EIGENID_STAGE1_LARGE_LAYOUT kWide
+#endif
+#define kStage1LargeLayout EIGENID_STAGE1_LARGE_LAYOUT
 constexpr int kStages = 5;  // stage1, stage2, lambda_A (side), bisect_minors, identity
 struct StageTimer {
   bool on = false, print = false;
@@ -391,16 +395,22 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   // Stage-1 layout (band.cu): wide (one 16-warp CTA per SM) for large n,
   // narrow (two 8-warp CTAs per SM) where the panel phases weigh more.
-  bool wide = n >= kStage1WideMinN;
-  // EIGENID_STAGE1_LAYOUT=wide|narrow overrides the choice (tests, A/B).
+  // wide8 (8 warps x 16 rows, one CTA per SM, 255 registers) replaces wide
+  // where it measured faster.
+  enum { kWide, kNarrow, kWide8 } layout = n >= kStage1WideMinN ? kStage1LargeLayout : kNarrow;
+  // EIGENID_STAGE1_LAYOUT=wide|narrow|wide8 overrides the choice (tests, A/B).
   if (const char* lay = std::getenv("EIGENID_STAGE1_LAYOUT")) {
-    if (std::strcmp(lay, "wide") == 0) wide = true;
-    if (std::strcmp(lay, "narrow") == 0) wide = false;
+    if (std::strcmp(lay, "wide") == 0) layout = kWide;
+    if (std::strcmp(lay, "narrow") == 0) layout = kNarrow;
+    if (std::strcmp(lay, "wide8") == 0) layout = kWide8;
   }
-  const int cps = wide ? wide::stage1_ctas_per_sm() : narrow::stage1_ctas_per_sm();
+  const int cps = layout == kWide    ? wide::stage1_ctas_per_sm()
+                  : layout == kWide8 ? wide8::stage1_ctas_per_sm()
+                                     : narrow::stage1_ctas_per_sm();
   auto launch1 = [&](const Stage1Args& a, int grid, cudaStream_t s, bool reset) {
-    return wide ? wide::launch_stage1(a, grid, s, reset)
-                : narrow::launch_stage1(a, grid, s, reset);
+    return layout == kWide    ? wide::launch_stage1(a, grid, s, reset)
+           : layout == kWide8 ? wide8::launch_stage1(a, grid, s, reset)
+                              : narrow::launch_stage1(a, grid, s, reset);
   };
   const int max_slots = sms * cps;
   // one SM's worth of slots is reserved for A's pipeline (then the helper)

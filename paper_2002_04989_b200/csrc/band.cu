@@ -39,14 +39,36 @@ constexpr int kB = 32;      // bandwidth / panel width
 #ifndef EIGENID_STAGE1_WIDE
 #define EIGENID_STAGE1_WIDE 1
 #endif
-constexpr int kNT = EIGENID_STAGE1_WIDE ? 512 : 256;  // threads per CTA
+// A third layout, "wide8" (EIGENID_STAGE1_RW = 2): 8 warps, one CTA per SM,
+// 128-row fused blocks with SIXTEEN rows per warp and up to 255 registers per
+// thread: every Bop / VT fragment read from shared memory feeds two DMMAs
+// instead of one and the transposed product shares its C fragment between
+// two X tiles, so the fused tile needs ~30 % fewer shared-memory wavefronts
+// (the L1 data pipe is the co-limiter of the 16-warp layouts).
+#ifndef EIGENID_STAGE1_RW
+#define EIGENID_STAGE1_RW 1
+#endif
+constexpr int kRW = EIGENID_STAGE1_RW;  // 8-row groups per warp in the fused pass
+// Interior-tile copy fast path and the skip of above-diagonal row groups:
+// both measured neutral-to-slower in the 16-warp layouts (already at the
+// 128-register cap: the extra live values spill), so they default to the
+// wide8 layout only.
+#ifndef EIGENID_FAST_STAGE
+#define EIGENID_FAST_STAGE (EIGENID_STAGE1_RW == 2)
+#endif
+#ifndef EIGENID_DIAG_SKIP
+#define EIGENID_DIAG_SKIP (EIGENID_STAGE1_RW == 2)
+#endif
+static_assert(kRW == 1 || (kRW == 2 && EIGENID_STAGE1_WIDE), "layout");
+constexpr int kNT = (EIGENID_STAGE1_WIDE && kRW == 1) ? 512 : 256;  // threads per CTA
 constexpr int kNW = kNT / 32;                         // warps per CTA
 constexpr int kCtasPerSm = EIGENID_STAGE1_WIDE ? 1 : 2;
 constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
 // Shared-memory layout (doubles); the GEMM region is reused by the panel /
 // Gram phases.  Every warp owns 8 rows of a GEMM-2 / fused row block.
-constexpr int kG2M = 8 * kNW, kG2N = 32, kG2K = 2 * kB;  // row block / tile / k
+constexpr int kG2M = 8 * kNW * kRW, kG2N = 32, kG2K = 2 * kB;  // fused row block / tile / k
+constexpr int kG2R = 8 * kNW;                          // GEMM 2 row block
 constexpr int kG1M = 64, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 68;
 constexpr int kMT1 = 8 * kG1M / kNT;                // 8-row m-tiles per warp
 constexpr int kG1_A = kG1M * kG1LDA;                // pass 1: A chunk 128 x 32
@@ -65,7 +87,7 @@ constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
 #endif
 constexpr int kFS = EIGENID_FUSED_STAGES;            // fused-pass stages
 constexpr int kXT = 16 / kNW;  // 8x8 tiles of the fused transposed product per warp
-constexpr int kG2St = kG2N * kG2K + kG2M * kG2N;    // Bop rows + C tile
+constexpr int kG2St = kG2N * kG2K + kG2R * kG2N;    // Bop rows + C tile
 #ifndef EIGENID_STAGE1_FUSED
 #define EIGENID_STAGE1_FUSED 1
 #endif
@@ -110,6 +132,10 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem,
   const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr),
                "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16_full(double* smem, const double* gmem) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
@@ -726,7 +752,7 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
   const int crow = 8 * warp + mm;  // this lane's row within the row block
-  for (int rb = 0; rb < s; rb += kG2M) {
+  for (int rb = 0; rb < s; rb += kG2R) {
     const int r = rb + crow;
     // k-pair q covers k = 8q .. 8q+7: lane kk takes k = 8q + 2kk in the
     // first DMMA of the pair and 8q + 2kk + 1 in the second, so both operands
@@ -741,7 +767,7 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
                                                      : V + (long long)r * kB + (k - kB));
       af[q] = make_double2(-v.x, -v.y);
     }
-    const int cend = min(rb + kG2M, s);
+    const int cend = min(rb + kG2R, s);
     const int ncb = min((cend + kG2N - 1) / kG2N, max_tiles);
     auto stage = [&](int ci) {
       if (ci < ncb) {
@@ -756,7 +782,7 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
           cp_async16(st + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
         }
         double* cs = st + kG2N * kG2K;
-        for (int t = tid; t < kG2M * (kG2N / 2); t += kNT) {
+        for (int t = tid; t < kG2R * (kG2N / 2); t += kNT) {
           const int row = t >> 4, c2 = (t & 15) * 2;
           const int gr = rb + row, gc = cb + c2;
           int bytes = 0;
@@ -858,12 +884,41 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
+// Arrival on an mbarrier triggered by the completion of every cp.async this
+// thread has issued so far (.noinc: it counts against the expected arrivals).
+__device__ __forceinline__ void cpa_mbar_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_inval(unsigned long long* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+// EIGENID_PIPE_MBAR: the fused pass's stage pipeline runs on mbarriers
+// instead of cp.async groups + a CTA barrier per tile.  "full[b]" (one
+// arrival per thread, triggered by the completion of its copies) tells a
+// warp that stage b holds its tile; "empty[b]" (one arrival per warp after
+// its transposed product) tells the copy issue that every warp is done with
+// stage b.  A warp that finishes a tile early starts the next tile's update
+// at once (it needs only data, not the other warps), and the next stage's
+// copies are issued after the update, when the stage they overwrite has long
+// been released: the only CTA-wide rendezvous left in a tile is the mid-tile
+// "C rows complete" mbarrier.
+#ifndef EIGENID_PIPE_MBAR
+#define EIGENID_PIPE_MBAR 1
+#endif
+static_assert(!EIGENID_PIPE_MBAR || (EIGENID_SPLIT_BAR && EIGENID_FUSED_STAGES == 2), "pipe");
+
 __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                            const double* Vp, const double* VTn, double* Xn,
                            double* sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
-  const int crow = 8 * warp + mm;
+  // this lane's rows within the row block: crow0 + 8 mt, mt < kRW
+  const int crow0 = 8 * kRW * warp + mm;
   double* sVr = sm + kFS * kFSt;
 #if EIGENID_SPLIT_BAR
   // "every warp's updated C rows are in shared memory": one arrival per warp
@@ -871,24 +926,42 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
   __shared__ alignas(8) unsigned long long cbar_storage;
   unsigned long long* cbar = &cbar_storage;
   unsigned cphase = 0;
+#if EIGENID_PIPE_MBAR
+  __shared__ alignas(8) unsigned long long pbar_storage[4];  // full[2], empty[2]
+  unsigned long long* const fullb = pbar_storage;
+  unsigned long long* const emptyb = pbar_storage + 2;
+  unsigned fbits = 0;  // bit b: parity of the next phase to wait for on full[b]
+  unsigned ebits = 0;  // bit b: phases begun on empty[b] (mod 2)
+  if (tid == 0) {
+    mbar_init(fullb, kNT);
+    mbar_init(fullb + 1, kNT);
+    mbar_init(emptyb, kNW);
+    mbar_init(emptyb + 1, kNW);
+  }
+#endif
   if (tid == 0) mbar_init(cbar, kNW);
   __syncthreads();
 #endif
   for (int rb = 0; rb < sn; rb += kG2M) {
-    const int r = rb + crow;
-    double2 af[kG2K / 8];
+    double2 af[kRW][kG2K / 8];
 #pragma unroll
-    for (int q = 0; q < kG2K / 8; ++q) {
-      const int k = 8 * q + 2 * kk;
-      double2 v = make_double2(0.0, 0.0);
-      if (r < sn)
-        v = *reinterpret_cast<const double2*>(k < kB ? W2p + (long long)r * kB + k
-                                                     : Vp + (long long)r * kB + (k - kB));
-      af[q] = make_double2(-v.x, -v.y);
+    for (int mt = 0; mt < kRW; ++mt) {
+      const int r = rb + crow0 + 8 * mt;
+#pragma unroll
+      for (int q = 0; q < kG2K / 8; ++q) {
+        const int k = 8 * q + 2 * kk;
+        double2 v = make_double2(0.0, 0.0);
+        if (r < sn)
+          v = *reinterpret_cast<const double2*>(k < kB ? W2p + (long long)r * kB + k
+                                                       : Vp + (long long)r * kB + (k - kB));
+        af[mt][q] = make_double2(-v.x, -v.y);
+      }
     }
-    double xr[kG2N / 8][2];
+    double xr[kRW][kG2N / 8][2];
 #pragma unroll
-    for (int nt = 0; nt < kG2N / 8; ++nt) xr[nt][0] = xr[nt][1] = 0.0;
+    for (int mt = 0; mt < kRW; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt) xr[mt][nt][0] = xr[mt][nt][1] = 0.0;
     const int cend = min(rb + kG2M, sn);
     const int ncb = (cend + kG2N - 1) / kG2N;
     auto stage = [&](int ci) {
@@ -920,8 +993,53 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           cp_async16(vc + row * kFVLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
                      bytes);
         }
+#if EIGENID_PIPE_MBAR
+        cpa_mbar_arrive(fullb + (ci % kFS));
+#endif
       }
+#if !EIGENID_PIPE_MBAR
       cpa_commit();
+#endif
+    };
+    // Interior row blocks (every row and column of every tile in range: all
+    // but the last partial block): each thread's copies of a tile sit at
+    // fixed offsets from three pointers that advance by one tile, so a stage
+    // is a handful of unpredicated cp.async off immediate offsets instead of
+    // ~230 instructions of index and predicate arithmetic.
+    const bool interior = EIGENID_FAST_STAGE && rb + kG2M <= sn;
+    auto stage_fast = [&](int ci) {
+      if (ci < ncb) {
+        constexpr int kBopIt = kG2N * (kG2K / 2) / kNT, kBopRows = kNT / 32;
+        constexpr int kCIt = kG2M * (kG2N / 2) / kNT, kCRows = kNT / 16;
+        constexpr int kVIt = kB * (kB / 2) / kNT;
+        static_assert(kBopRows % 2 == 0 && kCRows % 4 == 0, "swizzle terms must not change");
+        double* st = sm + (ci % kFS) * kFSt;
+        const long long off = (long long)ci * (kG2N * kB);  // cb * kB
+        const int brow = tid >> 5, bk2 = (tid & 31) * 2;
+        const double* bsrc =
+            (bk2 < kB ? Vp + bk2 : W2p + (bk2 - kB)) + off + (long long)brow * kB;
+        double* bdst = st + brow * kG2K + (bk2 ^ (8 * (brow & 1)));
+#pragma unroll
+        for (int i = 0; i < kBopIt; ++i)
+          cp_async16_full(bdst + i * kBopRows * kG2K, bsrc + i * kBopRows * kB);
+        const int crw = tid >> 4, cc2 = (tid & 15) * 2;
+        const double* csrc = A22n + (long long)(rb + crw) * ldw + ci * kG2N + cc2;
+        double* cdst = st + kG2N * kG2K + cswz(crw, cc2);
+#pragma unroll
+        for (int i = 0; i < kCIt; ++i)
+          cp_async16_full(cdst + i * kCRows * kG2N, csrc + (long long)i * kCRows * ldw);
+        const double* vsrc = VTn + off + (long long)crw * kB + cc2;
+        double* vdst = st + kG2N * kG2K + kG2M * kG2N + crw * kFVLD + cc2;
+#pragma unroll
+        for (int i = 0; i < kVIt; ++i)
+          cp_async16_full(vdst + i * kCRows * kFVLD, vsrc + i * kCRows * kB);
+#if EIGENID_PIPE_MBAR
+        cpa_mbar_arrive(fullb + (ci % kFS));
+#endif
+      }
+#if !EIGENID_PIPE_MBAR
+      cpa_commit();
+#endif
     };
     __syncthreads();  // the previous row block is done with every buffer
     for (int t = tid; t < kG2M * (kB / 2); t += kNT) {
@@ -932,7 +1050,12 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                  bytes);
     }
 #pragma unroll
-    for (int p = 0; p < kFS - 1; ++p) stage(p);
+    for (int p = 0; p < kFS - 1; ++p) {
+      if (interior)
+        stage_fast(p);
+      else
+        stage(p);
+    }
     // Tile body, specialised on whether the tile may cross the diagonal
     // (only then are the triangular masks needed).
     auto tile = [&](int ci, auto diag_tag) {
@@ -960,13 +1083,28 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           x2[u][0] = x2[u][1] = 0.0;
         }
       }
-      // ---- rank-2kB update of this lane's C row
-      double acc[kG2N / 8][2];
+      // A diagonal-crossing tile's rows above the diagonal (tile rows < d =
+      // cb - rb) hold only upper-triangle elements, which nothing reads: an
+      // 8-row group that lies wholly there skips its update and row product
+      // (their contributions are exact zeros), and the transposed product
+      // below starts at contraction row d.
+      const int dskip = (EIGENID_DIAG_SKIP && diag) ? cb - rb : 0;
+      bool live[kRW];
 #pragma unroll
-      for (int nt = 0; nt < kG2N / 8; ++nt) {
-        const double2 x = *reinterpret_cast<const double2*>(cs + cswz(crow, 8 * nt + 2 * kk));
-        acc[nt][0] = x.x;
-        acc[nt][1] = x.y;
+      for (int mt = 0; mt < kRW; ++mt)
+        live[mt] = !diag || 8 * kRW * warp + 8 * mt + 7 >= dskip;
+      // ---- rank-2kB update of this lane's C rows
+      double acc[kRW][kG2N / 8][2];
+#pragma unroll
+      for (int mt = 0; mt < kRW; ++mt) {
+        if (!live[mt]) continue;
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          const double2 x = *reinterpret_cast<const double2*>(
+              cs + cswz(crow0 + 8 * mt, 8 * nt + 2 * kk));
+          acc[mt][nt][0] = x.x;
+          acc[mt][nt][1] = x.y;
+        }
       }
 #pragma unroll
       for (int q = 0; q < kG2K / 8; ++q) {
@@ -975,24 +1113,53 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt)
           bf[nt] = *reinterpret_cast<const double2*>(b + (8 * nt + mm) * kG2K + kl);
-        // independent accumulators back to back (the DMMAs are volatile, so
-        // this order is the issue order)
+        // independent accumulators back to back
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].x, bf[nt].x);
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (!live[mt]) continue;
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], af[q].y, bf[nt].y);
+          for (int nt = 0; nt < kG2N / 8; ++nt)
+            dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][q].x, bf[nt].x);
+        }
+#pragma unroll
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (!live[mt]) continue;
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt)
+            dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][q].y, bf[nt].y);
+        }
       }
-#if EIGENID_SPLIT_BAR
-      // updated C rows to shared memory first, then arrive (non-blocking) on
-      // the "C tile complete" mbarrier (one arrival per warp), and run this
-      // warp's independent row product before waiting for the others: the
-      // DMMA pipe is fed across the barrier instead of draining at it
+      // updated C rows to shared memory for the transposed product
+      auto store_smem = [&]() {
 #pragma unroll
-      for (int nt = 0; nt < kG2N / 8; ++nt)
-        *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
-            make_double2(acc[nt][0], acc[nt][1]);
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (!live[mt]) continue;
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt)
+            *reinterpret_cast<double2*>(cs + cswz(crow0 + 8 * mt, 8 * nt + 2 * kk)) =
+                make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        }
+      };
+#if EIGENID_SPLIT_BAR
+      // store first, then arrive (non-blocking) on the "C tile complete"
+      // mbarrier (one arrival per warp), and run this warp's independent row
+      // product before waiting for the others: the DMMA pipe is fed across
+      // the barrier instead of draining at it
+      store_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(cbar);
+#if EIGENID_PIPE_MBAR
+      // next tile's copies: the stage they overwrite held tile ci-1, released
+      // by every warp after its transposed product (long ago by now)
+      if (ci + 1 < ncb) {
+        const int nb2 = (ci + 1) & 1;
+        if (ci >= 1) mbar_wait(emptyb + nb2, ((ebits >> nb2) & 1u) ^ 1u);
+        if (interior)
+          stage_fast(ci + 1);
+        else
+          stage(ci + 1);
+      }
+#endif
 #endif
       // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators: the
       // m8n8k4 accumulator of column tile q holds C[row][8q+2kk .. +1], which
@@ -1001,8 +1168,6 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
       for (int q = 0; q < kB / 8; ++q) {
         const int k = 8 * q + 2 * kk;
-        const double ax = (diag && cb + k > r) ? 0.0 : acc[q][0];
-        const double ay = (diag && cb + k + 1 > r) ? 0.0 : acc[q][1];
         double b0[kG2N / 8], b1[kG2N / 8];
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) {
@@ -1010,34 +1175,40 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           b1[nt] = vc[(k + 1) * kFVLD + 8 * nt + mm];
         }
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], ax, b0[nt]);
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (!live[mt]) continue;
+          const int r = rb + crow0 + 8 * mt;
+          const double ax = (diag && cb + k > r) ? 0.0 : acc[mt][q][0];
+          const double ay = (diag && cb + k + 1 > r) ? 0.0 : acc[mt][q][1];
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[nt][0], xr[nt][1], ay, b1[nt]);
+          for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[mt][nt][0], xr[mt][nt][1], ax, b0[nt]);
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[mt][nt][0], xr[mt][nt][1], ay, b1[nt]);
+        }
       }
-      auto store_c = [&]() {
+#pragma unroll
+      for (int mt = 0; mt < kRW; ++mt) {
+        if (!live[mt]) continue;
+        const int r = rb + crow0 + 8 * mt;
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) {
           const int col = cb + 8 * nt + 2 * kk;
           if (r < sn) {
             double* p = A22n + (long long)r * ldw + col;
             if (col + 1 < sn)
-              *reinterpret_cast<double2*>(p) = make_double2(acc[nt][0], acc[nt][1]);
+              *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
             else if (col < sn)
-              p[0] = acc[nt][0];
+              p[0] = acc[mt][nt][0];
           }
         }
-      };
-      store_c();
+      }
 #if EIGENID_SPLIT_BAR
 #ifndef EIGENID_EXP_NO_CBAR
       mbar_wait(cbar, cphase);
 #endif
       cphase ^= 1u;
 #else
-#pragma unroll
-      for (int nt = 0; nt < kG2N / 8; ++nt)
-        *reinterpret_cast<double2*>(cs + cswz(crow, 8 * nt + 2 * kk)) =
-            make_double2(acc[nt][0], acc[nt][1]);
+      store_smem();
       __syncthreads();
 #endif
       // ---- X[cb] += strict(C)^T VTn[rb]   (warp: X rows 8*mt2.., 8*kXT cols)
@@ -1045,7 +1216,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       {
         const int ccol = 8 * mt2 + mm;  // tile column of C = X row
 #pragma unroll 4
-        for (int k4 = 0; k4 < kG2M / 4; ++k4) {
+        for (int k4 = dskip / 4; k4 < kG2M / 4; ++k4) {
           const int krow = 4 * k4 + kk;  // tile row of C = contraction index
           const double v = cs[cswz(krow, ccol)];
           const double a = (diag && rb + krow <= cb + ccol) ? 0.0 : v;
@@ -1061,13 +1232,26 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         }
       }
 #endif
+#if EIGENID_PIPE_MBAR
+      __syncwarp();
+      if (lane == 0) mbar_arrive(emptyb + (ci & 1));
+      ebits ^= 1u << (ci & 1);
+#endif
     };
     for (int ci = 0; ci < ncb; ++ci) {
+#if EIGENID_PIPE_MBAR
+      mbar_wait(fullb + (ci & 1), (fbits >> (ci & 1)) & 1u);
+      fbits ^= 1u << (ci & 1);
+#else
       cpa_wait<kFS - 2>();
 #ifndef EIGENID_EXP_NO_TILE_SYNC
       __syncthreads();
 #endif
-      stage(ci + kFS - 1);
+      if (interior)
+        stage_fast(ci + kFS - 1);
+      else
+        stage(ci + kFS - 1);
+#endif
       if (ci * kG2N + kB > rb)
         tile(ci, std::true_type{});
       else
@@ -1076,18 +1260,30 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     // X[rb] += the row-part accumulators (after this row block's transposed
     // contributions to the same rows)
     __syncthreads();
-    if (r < sn) {
 #pragma unroll
-      for (int nt = 0; nt < kG2N / 8; ++nt) {
-        double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + 8 * nt + 2 * kk);
-        double2 x = *p;
-        x.x += xr[nt][0];
-        x.y += xr[nt][1];
-        *p = x;
+    for (int mt = 0; mt < kRW; ++mt) {
+      const int r = rb + crow0 + 8 * mt;
+      if (r < sn) {
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) {
+          double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + 8 * nt + 2 * kk);
+          double2 x = *p;
+          x.x += xr[mt][nt][0];
+          x.y += xr[mt][nt][1];
+          *p = x;
+        }
       }
     }
   }
   __syncthreads();
+#if EIGENID_SPLIT_BAR
+  if (tid == 0) {
+    mbar_inval(cbar);
+#if EIGENID_PIPE_MBAR
+    for (int b = 0; b < 4; ++b) mbar_inval(pbar_storage + b);
+#endif
+  }
+#endif
 }
 
 __device__ void write_band(const double* W, int ldw, int m, int c_begin,
