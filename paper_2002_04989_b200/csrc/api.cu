@@ -397,20 +397,23 @@ int run_large(eigenid_gpu_ctx* c, const double* dA, int n, int j0, int j1,
   // narrow (two 8-warp CTAs per SM) where the panel phases weigh more.
   // wide8 (8 warps x 16 rows, one CTA per SM, 255 registers) replaces wide
   // where it measured faster.
-  enum { kWide, kNarrow, kWide8 } layout = n >= kStage1WideMinN ? kStage1LargeLayout : kNarrow;
+  enum { kWide, kNarrow, kWide8, kWideSp } layout = n >= kStage1WideMinN ? kStage1LargeLayout : kNarrow;
   // EIGENID_STAGE1_LAYOUT=wide|narrow|wide8 overrides the choice (tests, A/B).
   if (const char* lay = std::getenv("EIGENID_STAGE1_LAYOUT")) {
     if (std::strcmp(lay, "wide") == 0) layout = kWide;
     if (std::strcmp(lay, "narrow") == 0) layout = kNarrow;
     if (std::strcmp(lay, "wide8") == 0) layout = kWide8;
+    if (std::strcmp(lay, "widesp") == 0) layout = kWideSp;
   }
-  const int cps = layout == kWide    ? wide::stage1_ctas_per_sm()
-                  : layout == kWide8 ? wide8::stage1_ctas_per_sm()
-                                     : narrow::stage1_ctas_per_sm();
+  const int cps = layout == kWide     ? wide::stage1_ctas_per_sm()
+                  : layout == kWide8  ? wide8::stage1_ctas_per_sm()
+                  : layout == kWideSp ? widesp::stage1_ctas_per_sm()
+                                      : narrow::stage1_ctas_per_sm();
   auto launch1 = [&](const Stage1Args& a, int grid, cudaStream_t s, bool reset) {
-    return layout == kWide    ? wide::launch_stage1(a, grid, s, reset)
-           : layout == kWide8 ? wide8::launch_stage1(a, grid, s, reset)
-                              : narrow::launch_stage1(a, grid, s, reset);
+    return layout == kWide     ? wide::launch_stage1(a, grid, s, reset)
+           : layout == kWide8  ? wide8::launch_stage1(a, grid, s, reset)
+           : layout == kWideSp ? widesp::launch_stage1(a, grid, s, reset)
+                               : narrow::launch_stage1(a, grid, s, reset);
   };
   const int max_slots = sms * cps;
   // one SM's worth of slots is reserved for A's pipeline (then the helper)

@@ -49,25 +49,43 @@ constexpr int kB = 32;      // bandwidth / panel width
 #define EIGENID_STAGE1_RW 1
 #endif
 constexpr int kRW = EIGENID_STAGE1_RW;  // 8-row groups per warp in the fused pass
-// Interior-tile copy fast path and the skip of above-diagonal row groups:
-// both measured neutral-to-slower in the 16-warp layouts (already at the
-// 128-register cap: the extra live values spill), so they default to the
-// wide8 layout only.
+// Interior-tile copy fast path: same-box -1.1 % (wide) / -12 % (wide8) at
+// n = 4096 with the mbarrier pipeline.  The skip of above-diagonal row groups
+// measured 2 % SLOWER in both layouts (the skipping warps only reach the
+// mid-tile barrier earlier) and stays off.
 #ifndef EIGENID_FAST_STAGE
-#define EIGENID_FAST_STAGE (EIGENID_STAGE1_RW == 2)
+#define EIGENID_FAST_STAGE 1
 #endif
 #ifndef EIGENID_DIAG_SKIP
-#define EIGENID_DIAG_SKIP (EIGENID_STAGE1_RW == 2)
+#define EIGENID_DIAG_SKIP 0
+#endif
+// unpredicated write-back of the updated C rows in interior row blocks
+#ifndef EIGENID_FAST_STORE
+#define EIGENID_FAST_STORE 1
 #endif
 static_assert(kRW == 1 || (kRW == 2 && EIGENID_STAGE1_WIDE), "layout");
-constexpr int kNT = (EIGENID_STAGE1_WIDE && kRW == 1) ? 512 : 256;  // threads per CTA
+// A fourth layout, "widesp" (EIGENID_STAGE1_SP = 1, with RW = 2): 16 warps and
+// one CTA per SM like "wide", but the fused pass is warp-specialised.  Warps
+// 0-7 compute with the wide8 tiling (sixteen rows per warp) after growing
+// their register allocation with setmaxnreg; warps 8-15 shrink theirs and
+// only issue the cp.async copies, running ahead of the compute warps through
+// the full / empty mbarriers.  Every other phase (panel, Gram, W2, GEMM 1/2)
+// uses all 16 warps at 128 registers.
+#ifndef EIGENID_STAGE1_SP
+#define EIGENID_STAGE1_SP 0
+#endif
+constexpr int kSP = EIGENID_STAGE1_SP;
+static_assert(!kSP || kRW == 2, "widesp uses the sixteen-rows-per-warp tiling");
+constexpr int kNT = (EIGENID_STAGE1_WIDE && (kRW == 1 || kSP)) ? 512 : 256;  // threads per CTA
 constexpr int kNW = kNT / 32;                         // warps per CTA
+constexpr int kCW = kSP ? kNW / 2 : kNW;              // warps that compute in the fused pass
+constexpr int kPT = kNT - 32 * kCW;                   // copy-only threads of the fused pass
 constexpr int kCtasPerSm = EIGENID_STAGE1_WIDE ? 1 : 2;
 constexpr int kLDAB = 2 * kB + 1;  // band storage: diagonals 0..2kB per column
 
 // Shared-memory layout (doubles); the GEMM region is reused by the panel /
 // Gram phases.  Every warp owns 8 rows of a GEMM-2 / fused row block.
-constexpr int kG2M = 8 * kNW * kRW, kG2N = 32, kG2K = 2 * kB;  // fused row block / tile / k
+constexpr int kG2M = 8 * kCW * kRW, kG2N = 32, kG2K = 2 * kB;  // fused row block / tile / k
 constexpr int kG2R = 8 * kNW;                          // GEMM 2 row block
 constexpr int kG1M = 64, kG1K = 32, kG1LDA = 36, kG1LDB = 36, kG1TLD = 68;
 constexpr int kMT1 = 8 * kG1M / kNT;                // 8-row m-tiles per warp
@@ -86,7 +104,7 @@ constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
 #define EIGENID_FUSED_STAGES 2
 #endif
 constexpr int kFS = EIGENID_FUSED_STAGES;            // fused-pass stages
-constexpr int kXT = 16 / kNW;  // 8x8 tiles of the fused transposed product per warp
+constexpr int kXT = 16 / kCW;  // 8x8 tiles of the fused transposed product per warp
 constexpr int kG2St = kG2N * kG2K + kG2R * kG2N;    // Bop rows + C tile
 #ifndef EIGENID_STAGE1_FUSED
 #define EIGENID_STAGE1_FUSED 1
@@ -910,8 +928,12 @@ __device__ __forceinline__ void mbar_inval(unsigned long long* bar) {
 #ifndef EIGENID_PIPE_MBAR
 #define EIGENID_PIPE_MBAR 1
 #endif
-static_assert(!EIGENID_PIPE_MBAR || (EIGENID_SPLIT_BAR && EIGENID_FUSED_STAGES == 2), "pipe");
+#ifndef EIGENID_ISSUE_POINT
+#define EIGENID_ISSUE_POINT 0
+#endif
+static_assert(!EIGENID_PIPE_MBAR || EIGENID_SPLIT_BAR, "pipe");
 
+#if !EIGENID_STAGE1_SP
 __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                            const double* Vp, const double* VTn, double* Xn,
                            double* sm) {
@@ -927,16 +949,16 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
   unsigned long long* cbar = &cbar_storage;
   unsigned cphase = 0;
 #if EIGENID_PIPE_MBAR
-  __shared__ alignas(8) unsigned long long pbar_storage[4];  // full[2], empty[2]
+  __shared__ alignas(8) unsigned long long pbar_storage[2 * kFS];  // full[], empty[]
   unsigned long long* const fullb = pbar_storage;
-  unsigned long long* const emptyb = pbar_storage + 2;
+  unsigned long long* const emptyb = pbar_storage + kFS;
   unsigned fbits = 0;  // bit b: parity of the next phase to wait for on full[b]
   unsigned ebits = 0;  // bit b: phases begun on empty[b] (mod 2)
   if (tid == 0) {
-    mbar_init(fullb, kNT);
-    mbar_init(fullb + 1, kNT);
-    mbar_init(emptyb, kNW);
-    mbar_init(emptyb + 1, kNW);
+    for (int b = 0; b < kFS; ++b) {
+      mbar_init(fullb + b, kNT);
+      mbar_init(emptyb + b, kNW);
+    }
   }
 #endif
   if (tid == 0) mbar_init(cbar, kNW);
@@ -1006,7 +1028,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     // fixed offsets from three pointers that advance by one tile, so a stage
     // is a handful of unpredicated cp.async off immediate offsets instead of
     // ~230 instructions of index and predicate arithmetic.
-    const bool interior = EIGENID_FAST_STAGE && rb + kG2M <= sn;
+    const bool interior = rb + kG2M <= sn;
     auto stage_fast = [&](int ci) {
       if (ci < ncb) {
         constexpr int kBopIt = kG2N * (kG2K / 2) / kNT, kBopRows = kNT / 32;
@@ -1051,7 +1073,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     }
 #pragma unroll
     for (int p = 0; p < kFS - 1; ++p) {
-      if (interior)
+      if (EIGENID_FAST_STAGE && interior)
         stage_fast(p);
       else
         stage(p);
@@ -1149,16 +1171,23 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       __syncwarp();
       if (lane == 0) mbar_arrive(cbar);
 #if EIGENID_PIPE_MBAR
-      // next tile's copies: the stage they overwrite held tile ci-1, released
-      // by every warp after its transposed product (long ago by now)
-      if (ci + 1 < ncb) {
-        const int nb2 = (ci + 1) & 1;
-        if (ci >= 1) mbar_wait(emptyb + nb2, ((ebits >> nb2) & 1u) ^ 1u);
-        if (interior)
-          stage_fast(ci + 1);
-        else
-          stage(ci + 1);
-      }
+      // copies of tile ci + kFS - 1: the stage they overwrite held tile ci-1,
+      // released by every warp after its transposed product (long ago by now)
+      auto issue_next = [&]() {
+        if (ci + kFS - 1 < ncb) {
+          const int nb2 = (ci + kFS - 1) % kFS;
+          if (ci >= 1) mbar_wait(emptyb + nb2, ((ebits >> nb2) & 1u) ^ 1u);
+          if (EIGENID_FAST_STAGE && interior)
+            stage_fast(ci + kFS - 1);
+          else
+            stage(ci + kFS - 1);
+        }
+      };
+      // EIGENID_ISSUE_POINT: 0 = here (before the row product), 1 = after the
+      // row product, 2 = half of the warps of each SM sub-partition at each
+      const bool issue_early = EIGENID_ISSUE_POINT == 0 ||
+                               (EIGENID_ISSUE_POINT == 2 && ((warp >> 2) & 1) == 0);
+      if (issue_early) issue_next();
 #endif
 #endif
       // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators: the
@@ -1186,22 +1215,37 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           for (int nt = 0; nt < kG2N / 8; ++nt) dmma(xr[mt][nt][0], xr[mt][nt][1], ay, b1[nt]);
         }
       }
+      if (EIGENID_FAST_STORE && interior) {  // every row and column in range
 #pragma unroll
-      for (int mt = 0; mt < kRW; ++mt) {
-        if (!live[mt]) continue;
-        const int r = rb + crow0 + 8 * mt;
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (!live[mt]) continue;
+          double* p = A22n + (long long)(rb + crow0 + 8 * mt) * ldw + cb + 2 * kk;
 #pragma unroll
-        for (int nt = 0; nt < kG2N / 8; ++nt) {
-          const int col = cb + 8 * nt + 2 * kk;
-          if (r < sn) {
-            double* p = A22n + (long long)r * ldw + col;
-            if (col + 1 < sn)
-              *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-            else if (col < sn)
-              p[0] = acc[mt][nt][0];
+          for (int nt = 0; nt < kG2N / 8; ++nt)
+            *reinterpret_cast<double2*>(p + 8 * nt) =
+                make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        }
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (!live[mt]) continue;
+          const int r = rb + crow0 + 8 * mt;
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt) {
+            const int col = cb + 8 * nt + 2 * kk;
+            if (r < sn) {
+              double* p = A22n + (long long)r * ldw + col;
+              if (col + 1 < sn)
+                *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+              else if (col < sn)
+                p[0] = acc[mt][nt][0];
+            }
           }
         }
       }
+#if EIGENID_PIPE_MBAR
+      if (!issue_early) issue_next();
+#endif
 #if EIGENID_SPLIT_BAR
 #ifndef EIGENID_EXP_NO_CBAR
       mbar_wait(cbar, cphase);
@@ -1234,20 +1278,20 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #endif
 #if EIGENID_PIPE_MBAR
       __syncwarp();
-      if (lane == 0) mbar_arrive(emptyb + (ci & 1));
-      ebits ^= 1u << (ci & 1);
+      if (lane == 0) mbar_arrive(emptyb + (ci % kFS));
+      ebits ^= 1u << (ci % kFS);
 #endif
     };
     for (int ci = 0; ci < ncb; ++ci) {
 #if EIGENID_PIPE_MBAR
-      mbar_wait(fullb + (ci & 1), (fbits >> (ci & 1)) & 1u);
-      fbits ^= 1u << (ci & 1);
+      mbar_wait(fullb + (ci % kFS), (fbits >> (ci % kFS)) & 1u);
+      fbits ^= 1u << (ci % kFS);
 #else
       cpa_wait<kFS - 2>();
 #ifndef EIGENID_EXP_NO_TILE_SYNC
       __syncthreads();
 #endif
-      if (interior)
+      if (EIGENID_FAST_STAGE && interior)
         stage_fast(ci + kFS - 1);
       else
         stage(ci + kFS - 1);
@@ -1280,11 +1324,426 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
   if (tid == 0) {
     mbar_inval(cbar);
 #if EIGENID_PIPE_MBAR
-    for (int b = 0; b < 4; ++b) mbar_inval(pbar_storage + b);
+    for (int b = 0; b < 2 * kFS; ++b) mbar_inval(pbar_storage + b);
 #endif
   }
 #endif
 }
+
+#else  // EIGENID_STAGE1_SP
+template <int N>
+__device__ __forceinline__ void reg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+// barrier over the compute warps only
+__device__ __forceinline__ void bar_compute() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kCW) : "memory");
+}
+#ifndef EIGENID_SP_SKIP
+#define EIGENID_SP_SKIP 0
+#endif
+#ifndef EIGENID_SP_REGS_COMPUTE
+#define EIGENID_SP_REGS_COMPUTE 216
+#endif
+constexpr int kRegCompute = EIGENID_SP_REGS_COMPUTE;
+constexpr int kRegCopy = (65536 - 32 * kCW * kRegCompute) / kPT / 8 * 8;
+static_assert(kRegCopy >= 24 && kRegCompute <= 232, "setmaxnreg split");
+
+// Warp-specialised fused pass (same mathematics and accumulation orders as
+// the generic one above).  Tiles are numbered g = 0, 1, ... across the row
+// blocks of the pass and live in stage g % kFS.
+//   copy warps:    wait empty[g % kFS] (tile g - kFS released), issue the
+//                  tile's copies, arrive on full[g % kFS] when they land; the
+//                  row block's VTn[rb] rows follow its first tile, once the
+//                  compute warps are done with the previous row block
+//                  (rbdone), and arrive on svr_full.
+//   compute warps: wait full, update, arrive cbar, row product, wait cbar,
+//                  (first tile: wait svr_full), transposed product, arrive
+//                  empty.  Two compute-warp barriers per row block order the
+//                  X read-modify-writes.
+__device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
+                           const double* Vp, const double* VTn, double* Xn,
+                           double* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* sVr = sm + kFS * kFSt;
+  __shared__ alignas(8) unsigned long long bars[2 * kFS + 3];
+  unsigned long long* const fullb = bars;
+  unsigned long long* const emptyb = bars + kFS;
+  unsigned long long* const cbar = bars + 2 * kFS;
+  unsigned long long* const svr_full = cbar + 1;
+  unsigned long long* const rbdone = cbar + 2;
+  if (tid == 0) {
+    for (int b = 0; b < kFS; ++b) {
+      mbar_init(fullb + b, kPT);
+      mbar_init(emptyb + b, kCW);
+    }
+    mbar_init(cbar, kCW);
+    mbar_init(svr_full, kPT);
+    mbar_init(rbdone, kCW);
+  }
+  __syncthreads();
+  if (warp >= kCW) {
+    // ------------------------------------------------------- copy warps
+    reg_dec<kRegCopy>();
+    const int pt = tid - 32 * kCW;
+    int g = 0;
+    unsigned ebits = 0, rbpar = 0;
+    for (int rb = 0; rb < sn; rb += kG2M) {
+      const int cend = min(rb + kG2M, sn);
+      const int ncb = (cend + kG2N - 1) / kG2N;
+      const bool interior = rb + kG2M <= sn;
+      for (int ci = 0; ci < ncb; ++ci, ++g) {
+        const int sb = g % kFS;
+        if (g >= kFS) {
+          mbar_wait(emptyb + sb, (ebits >> sb) & 1u);
+          ebits ^= 1u << sb;
+        }
+        double* st = sm + sb * kFSt;
+        const int cb = ci * kG2N;
+#ifdef EIGENID_EXP_NO_COPY
+        if (false) {
+        } else if (false) {
+#else
+        if (interior) {
+#endif
+          constexpr int kBopIt = kG2N * (kG2K / 2) / kPT, kBopRows = kPT / 32;
+          constexpr int kCIt = kG2M * (kG2N / 2) / kPT, kCRows = kPT / 16;
+          constexpr int kVIt = kB * (kB / 2) / kPT;
+          static_assert(kBopRows % 2 == 0 && kCRows % 4 == 0, "swizzle terms must not change");
+          const long long off = (long long)cb * kB;
+          const int brow = pt >> 5, bk2 = (pt & 31) * 2;
+          const double* bsrc =
+              (bk2 < kB ? Vp + bk2 : W2p + (bk2 - kB)) + off + (long long)brow * kB;
+          double* bdst = st + brow * kG2K + (bk2 ^ (8 * (brow & 1)));
+#pragma unroll
+          for (int i = 0; i < kBopIt; ++i)
+            cp_async16_full(bdst + i * kBopRows * kG2K, bsrc + i * kBopRows * kB);
+          const int crw = pt >> 4, cc2 = (pt & 15) * 2;
+          const double* csrc = A22n + (long long)(rb + crw) * ldw + cb + cc2;
+          double* cdst = st + kG2N * kG2K + cswz(crw, cc2);
+#pragma unroll
+          for (int i = 0; i < kCIt; ++i)
+            cp_async16_full(cdst + i * kCRows * kG2N, csrc + (long long)i * kCRows * ldw);
+          const double* vsrc = VTn + off + (long long)crw * kB + cc2;
+          double* vdst = st + kG2N * kG2K + kG2M * kG2N + crw * kFVLD + cc2;
+#pragma unroll
+          for (int i = 0; i < kVIt; ++i)
+            cp_async16_full(vdst + i * kCRows * kFVLD, vsrc + i * kCRows * kB);
+        } else
+#ifdef EIGENID_EXP_NO_COPY
+            if (false)
+#endif
+        {
+          for (int t = pt; t < kG2N * (kG2K / 2); t += kPT) {
+            const int row = t >> 5, k2 = (t & 31) * 2;
+            const int gr = cb + row;
+            const int bytes = gr < sn ? 16 : 0;
+            const long long gg = (long long)(bytes ? gr : 0) * kB;
+            const double* src = k2 < kB ? Vp + gg + k2 : W2p + gg + (k2 - kB);
+            cp_async16(st + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
+          }
+          double* cs = st + kG2N * kG2K;
+          for (int t = pt; t < kG2M * (kG2N / 2); t += kPT) {
+            const int row = t >> 4, c2 = (t & 15) * 2;
+            const int gr = rb + row, gc = cb + c2;
+            int bytes = 0;
+            if (gr < sn && gc < sn) bytes = gc + 1 < sn ? 16 : 8;
+            cp_async16(cs + cswz(row, c2), bytes ? A22n + (long long)gr * ldw + gc : A22n,
+                       bytes);
+          }
+          double* vc = cs + kG2M * kG2N;
+          for (int t = pt; t < kB * (kB / 2); t += kPT) {
+            const int row = t >> 4, c2 = (t & 15) * 2;
+            const int gr = cb + row;
+            const int bytes = gr < sn ? 16 : 0;
+            cp_async16(vc + row * kFVLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
+                       bytes);
+          }
+        }
+        cpa_mbar_arrive(fullb + sb);
+        if (ci == 0) {
+          // VTn[rb] rows: the compute warps must be done with the previous
+          // row block's transposed products
+          if (rb > 0) {
+            mbar_wait(rbdone, rbpar);
+            rbpar ^= 1u;
+          }
+          for (int t = pt; t < kG2M * (kB / 2); t += kPT) {
+            const int row = t >> 4, c2 = (t & 15) * 2;
+            const int gr = rb + row;
+            const int bytes = gr < sn ? 16 : 0;
+            cp_async16(sVr + row * kFVRLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
+                       bytes);
+          }
+          cpa_mbar_arrive(svr_full);
+        }
+      }
+    }
+    cpa_wait0();
+  } else {
+    // ---------------------------------------------------- compute warps
+    reg_inc<kRegCompute>();
+    const int kk = lane & 3, mm = lane >> 2;
+    // 8-row group mt of this warp is group warp + kCW mt of the row block
+    // (interleaved, so the dead groups of a diagonal or tail tile are spread
+    // evenly over the SM sub-partitions)
+    int crow[kRW];
+#pragma unroll
+    for (int mt = 0; mt < kRW; ++mt) crow[mt] = 8 * (warp + kCW * mt) + mm;
+    int g = 0;
+    unsigned fbits = 0, cphase = 0, svphase = 0;
+    for (int rb = 0; rb < sn; rb += kG2M) {
+      double2 af[kRW][kG2K / 8];
+#pragma unroll
+      for (int mt = 0; mt < kRW; ++mt) {
+        const int r = rb + crow[mt];
+#pragma unroll
+        for (int q = 0; q < kG2K / 8; ++q) {
+          const int k = 8 * q + 2 * kk;
+          double2 v = make_double2(0.0, 0.0);
+          if (r < sn)
+            v = *reinterpret_cast<const double2*>(k < kB ? W2p + (long long)r * kB + k
+                                                         : Vp + (long long)r * kB + (k - kB));
+          af[mt][q] = make_double2(-v.x, -v.y);
+        }
+      }
+      double xr[kRW][kG2N / 8][2];
+#pragma unroll
+      for (int mt = 0; mt < kRW; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < kG2N / 8; ++nt) xr[mt][nt][0] = xr[mt][nt][1] = 0.0;
+      const int cend = min(rb + kG2M, sn);
+      const int ncb = (cend + kG2N - 1) / kG2N;
+      const bool interior = rb + kG2M <= sn;
+      double x2n[kXT][2];
+      auto load_x2 = [&](int ci) {
+        const int xr0 = ci * kG2N + 8 * (warp / (4 / kXT)) + mm;
+#pragma unroll
+        for (int u = 0; u < kXT; ++u) {
+          const int xc = 8 * ((warp % (4 / kXT)) * kXT + u) + 2 * kk;
+#if defined(EIGENID_EXP_NO_XRMW) || defined(EIGENID_EXP_NO_XLOAD)
+          if (xr0 < 0) {
+#else
+          if (xr0 < sn) {
+#endif
+            double2 t;
+            asm volatile("ld.global.v2.f64 {%0, %1}, [%2];\n"
+                         : "=d"(t.x), "=d"(t.y)
+                         : "l"(Xn + (long long)xr0 * kB + xc));
+            x2n[u][0] = t.x;
+            x2n[u][1] = t.y;
+          } else {
+            x2n[u][0] = x2n[u][1] = 0.0;
+          }
+        }
+      };
+      load_x2(0);
+      auto tile = [&](int ci, auto diag_tag) {
+        constexpr bool diag = decltype(diag_tag)::value;
+        const int cb = ci * kG2N;
+        const int sb = g % kFS;
+        const double* b = sm + sb * kFSt;
+        double* cs = const_cast<double*>(b) + kG2N * kG2K;
+        const double* vc = cs + kG2M * kG2N;
+        // X[cb] block of this warp for the transposed product: prefetched
+        // one tile ahead (nothing else touches those rows of X during this
+        // row block), the first tile's at the top of the row block
+        const int mt2 = warp / (4 / kXT), nb = (warp % (4 / kXT)) * kXT;
+        const int xrow = cb + 8 * mt2 + mm;
+        double x2[kXT][2];
+#pragma unroll
+        for (int u = 0; u < kXT; ++u) {
+          x2[u][0] = x2n[u][0];
+          x2[u][1] = x2n[u][1];
+        }
+        if (ci + 1 < ncb) load_x2(ci + 1);
+        mbar_wait(fullb + sb, (fbits >> sb) & 1u);
+        fbits ^= 1u << sb;
+        // Slow-path tiles (diagonal-crossing, or any tile of the last partial
+        // row block): an 8-row group wholly above the diagonal (tile rows < d
+        // = cb - rb hold only upper-triangle elements, which nothing reads)
+        // or wholly past the last row skips its update and row product
+        // (exact zeros), and the transposed product runs over the contraction
+        // rows [d, rows in range) only.
+        const int dskip = (EIGENID_SP_SKIP && diag) ? max(cb - rb, 0) : 0;
+        const int kend4 = (EIGENID_SP_SKIP && diag) ? (min(kG2M, sn - rb) + 3) / 4 : kG2M / 4;
+        bool live[kRW];
+#pragma unroll
+        for (int mt = 0; mt < kRW; ++mt)
+          live[mt] = !(EIGENID_SP_SKIP && diag) ||
+                     (8 * (warp + kCW * mt) + 7 >= dskip && rb + 8 * (warp + kCW * mt) < sn);
+        // ---- rank-2kB update of this lane's C rows
+        double acc[kRW][kG2N / 8][2];
+#pragma unroll
+        for (int mt = 0; mt < kRW; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt) {
+            const double2 x = *reinterpret_cast<const double2*>(
+                cs + cswz(crow[mt], 8 * nt + 2 * kk));
+            acc[mt][nt][0] = x.x;
+            acc[mt][nt][1] = x.y;
+          }
+#pragma unroll
+        for (int q = 0; q < kG2K / 8; ++q) {
+          const int kl = (8 * q + 2 * kk) ^ (8 * (mm & 1));
+          double2 bf[kG2N / 8];
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt)
+            bf[nt] = *reinterpret_cast<const double2*>(b + (8 * nt + mm) * kG2K + kl);
+#pragma unroll
+          for (int mt = 0; mt < kRW; ++mt) {
+            if (!live[mt]) continue;
+#pragma unroll
+            for (int nt = 0; nt < kG2N / 8; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][q].x, bf[nt].x);
+          }
+#pragma unroll
+          for (int mt = 0; mt < kRW; ++mt) {
+            if (!live[mt]) continue;
+#pragma unroll
+            for (int nt = 0; nt < kG2N / 8; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][q].y, bf[nt].y);
+          }
+        }
+        // updated C rows to shared memory, arrive, row product, then wait
+#pragma unroll
+        for (int mt = 0; mt < kRW; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt)
+            *reinterpret_cast<double2*>(cs + cswz(crow[mt], 8 * nt + 2 * kk)) =
+                make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(cbar);
+        // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators
+#pragma unroll
+        for (int q = 0; q < kB / 8; ++q) {
+          const int k = 8 * q + 2 * kk;
+          double b0[kG2N / 8], b1[kG2N / 8];
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt) {
+            b0[nt] = vc[k * kFVLD + 8 * nt + mm];
+            b1[nt] = vc[(k + 1) * kFVLD + 8 * nt + mm];
+          }
+#pragma unroll
+          for (int mt = 0; mt < kRW; ++mt) {
+            if (!live[mt]) continue;
+            const int r = rb + crow[mt];
+            const double ax = (diag && cb + k > r) ? 0.0 : acc[mt][q][0];
+            const double ay = (diag && cb + k + 1 > r) ? 0.0 : acc[mt][q][1];
+#pragma unroll
+            for (int nt = 0; nt < kG2N / 8; ++nt)
+              dmma(xr[mt][nt][0], xr[mt][nt][1], ax, b0[nt]);
+#pragma unroll
+            for (int nt = 0; nt < kG2N / 8; ++nt)
+              dmma(xr[mt][nt][0], xr[mt][nt][1], ay, b1[nt]);
+          }
+        }
+#ifdef EIGENID_EXP_NO_STORE
+        if (sn < 0) {
+#else
+        if (EIGENID_FAST_STORE && interior) {  // every row and column in range
+#endif
+#pragma unroll
+          for (int mt = 0; mt < kRW; ++mt) {
+            double* p = A22n + (long long)(rb + crow[mt]) * ldw + cb + 2 * kk;
+#pragma unroll
+            for (int nt = 0; nt < kG2N / 8; ++nt)
+              *reinterpret_cast<double2*>(p + 8 * nt) =
+                  make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          }
+        } else {
+#pragma unroll
+          for (int mt = 0; mt < kRW; ++mt) {
+            const int r = rb + crow[mt];
+#pragma unroll
+            for (int nt = 0; nt < kG2N / 8; ++nt) {
+              const int col = cb + 8 * nt + 2 * kk;
+              if (r < sn) {
+                double* p = A22n + (long long)r * ldw + col;
+                if (col + 1 < sn)
+                  *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+                else if (col < sn)
+                  p[0] = acc[mt][nt][0];
+              }
+            }
+          }
+        }
+        mbar_wait(cbar, cphase);
+        cphase ^= 1u;
+        if (ci == 0) {  // this row block's VTn[rb] rows have landed
+          mbar_wait(svr_full, svphase);
+          svphase ^= 1u;
+        }
+        // ---- X[cb] += strict(C)^T VTn[rb]
+        {
+          const int ccol = 8 * mt2 + mm;
+#pragma unroll 4
+          for (int k4 = dskip / 4; k4 < kend4; ++k4) {
+            const int krow = 4 * k4 + kk;
+            const double v = cs[cswz(krow, ccol)];
+            const double a = (diag && rb + krow <= cb + ccol) ? 0.0 : v;
+#pragma unroll
+            for (int u = 0; u < kXT; ++u)
+              dmma(x2[u][0], x2[u][1], a, sVr[krow * kFVRLD + 8 * (nb + u) + mm]);
+          }
+#if defined(EIGENID_EXP_NO_XRMW) || defined(EIGENID_EXP_NO_XSTORE)
+          if (xrow < 0) {
+#else
+          if (xrow < sn) {
+#endif
+#pragma unroll
+            for (int u = 0; u < kXT; ++u)
+              *reinterpret_cast<double2*>(Xn + (long long)xrow * kB + 8 * (nb + u) + 2 * kk) =
+                  make_double2(x2[u][0], x2[u][1]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(emptyb + sb);
+        ++g;
+      };
+      for (int ci = 0; ci < ncb; ++ci) {
+        if (ci * kG2N + kB > rb || (EIGENID_SP_SKIP && !interior))
+          tile(ci, std::true_type{});
+        else
+          tile(ci, std::false_type{});
+      }
+      // the copy warps may now overwrite VTn[rb]
+      __syncwarp();
+      if (lane == 0) mbar_arrive(rbdone);
+      // X[rb] += the row-part accumulators, after this row block's transposed
+      // contributions to the same rows and before the next row block's
+      bar_compute();
+#pragma unroll
+      for (int mt = 0; mt < kRW; ++mt) {
+        const int r = rb + crow[mt];
+        if (r < sn) {
+#pragma unroll
+          for (int nt = 0; nt < kG2N / 8; ++nt) {
+            double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + 8 * nt + 2 * kk);
+            double2 x = *p;
+            x.x += xr[mt][nt][0];
+            x.y += xr[mt][nt][1];
+            *p = x;
+          }
+        }
+      }
+      bar_compute();
+    }
+    reg_dec<128>();
+  }
+  if (warp >= kCW) reg_inc<128>();
+#ifndef EIGENID_SP_NO_MERGE_DEC
+  reg_dec<128>();  // every warp is back at 128: tell the register allocator so
+#endif
+  __syncthreads();
+  if (tid == 0)
+    for (int b = 0; b < 2 * kFS + 3; ++b) mbar_inval(bars + b);
+}
+#endif  // EIGENID_STAGE1_SP
 
 __device__ void write_band(const double* W, int ldw, int m, int c_begin,
                            int c_end, double* band) {

@@ -56,6 +56,11 @@ cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st,
                           bool reset = true);
 int stage1_ctas_per_sm();
 }  // namespace wide8
+namespace widesp {
+cudaError_t launch_stage1(const Stage1Args& a, int grid, cudaStream_t st,
+                          bool reset = true);
+int stage1_ctas_per_sm();
+}  // namespace widesp
 int stage1_band_ld();
 int stage1_bandwidth();
 long long stage1_ws_doubles(int n, int ldw);  // per-slot workspace

@@ -3,6 +3,7 @@
 #   VARIANTS='base: ;wide:-DEIGENID_STAGE1_WIDE=1' N=4096 R=591 REPS=2 bash tools/ab_variants.sh
 # A variant spec may end in '|<dir>': sources present in <dir> replace the
 # in-tree ones of the same name (e.g. an older kernel file for a same-box A/B).
+# LAYOUT=wide|narrow|wide8 picks the stage-1 layout (default: by n).
 # Each variant is built into /tmp/ab_<name> and timed with tools/prof_minors.py
 # (lambda(A) + R minor spectra); per-stage device times go to gpurun_out/ab.log.
 cd $GRAFT_REPO_ROOT
@@ -30,7 +31,7 @@ wait
 for rep in $(seq $REPS); do
   for name in "${names[@]}"; do
     echo "== $name" >> gpurun_out/ab.log
-    EIGENID_LIB=/tmp/ab_$name/libeigenid_b200.so EIGENID_PROFILE=1 timeout 300 \
+    EIGENID_STAGE1_LAYOUT=${LAYOUT:-} EIGENID_LIB=/tmp/ab_$name/libeigenid_b200.so EIGENID_PROFILE=1 timeout 300 \
       python tools/prof_minors.py $N $R >> gpurun_out/ab.log 2>&1
   done
 done
