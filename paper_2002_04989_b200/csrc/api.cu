@@ -312,7 +312,7 @@ int nccl_fail(eigenid_gpu_err* err, ncclResult_t r, const char* where) {
 // narrow one at n = 1024.
 constexpr int kStage1WideMinN = 3072;
 #ifndef EIGENID_STAGE1_LARGE_LAYOUT
-#define EIGENID_STAGE1_LARGE_LAYOUT kWide
+#define EIGENID_STAGE1_LARGE_LAYOUT kWideSp
 #endif
 #define kStage1LargeLayout EIGENID_STAGE1_LARGE_LAYOUT
 constexpr int kStages = 5;  // stage1, stage2, lambda_A (side), bisect_minors, identity

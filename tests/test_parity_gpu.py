@@ -202,24 +202,32 @@ def test_chunked_memory_plan_is_bit_identical(engine, oracle, monkeypatch):
 
 @pytest.mark.parametrize("n", [300, 1031])
 def test_stage1_layouts_agree(engine, oracle, monkeypatch, n):
-    """Both compiled stage-1 layouts (wide: one 16-warp CTA per SM; narrow:
-    two 8-warp CTAs per SM) reduce the same minors; they differ only in the
-    rounding order of the trailing updates, so their spectra agree to a few
-    ulps of ||A|| and each matches the oracle."""
+    """The four compiled stage-1 layouts (wide: one 16-warp CTA per SM;
+    narrow: two 8-warp CTAs per SM; wide8: one 8-warp CTA with sixteen rows
+    per warp; widesp: 16 warps with a warp-specialised fused pass) reduce the
+    same minors.  The fused pass accumulates every element in the same order
+    in all of them, so widesp (16-warp panel phases) is bit-identical to wide;
+    the 8-warp layouts differ from it only in the rounding order of the panel
+    Gram sums, so their spectra agree to a few ulps of ||A||.  Each matches
+    the oracle."""
     a = oracle.random_symmetric(5, n) * np.sqrt(2.0 / n)
     rows = [0, n // 2, n - 1]
     got = {}
-    for lay in ("wide", "narrow"):
+    for lay in ("wide", "narrow", "wide8", "widesp"):
         monkeypatch.setenv("EIGENID_STAGE1_LAYOUT", lay)
         got[lay] = engine.minor_spectra(a, 0, n)
     monkeypatch.delenv("EIGENID_STAGE1_LAYOUT")
-    (lw, mw), (ln, mn) = got["wide"], got["narrow"]
-    assert np.max(np.abs(lw - ln)) <= 1e-13
-    assert np.max(np.abs(mw - mn)) <= 1e-13
+    lw, mw = got["wide"]
+    for x, y in zip(got["widesp"], got["wide"]):
+        assert np.array_equal(bits(x), bits(y))
+    for lay in ("narrow", "wide8"):
+        ln, mn = got[lay]
+        assert np.max(np.abs(lw - ln)) <= 1e-13, lay
+        assert np.max(np.abs(mw - mn)) <= 1e-13, lay
     for j in rows:
         want = oracle.eigenvalues(oracle.minor(a, j))
-        assert np.max(np.abs(mw[j] - want)) <= 1e-13
-        assert np.max(np.abs(mn[j] - want)) <= 1e-13
+        for lay in got:
+            assert np.max(np.abs(got[lay][1][j] - want)) <= 1e-13, (lay, j)
 
 
 def test_stage2_warp_counts_bit_identical(engine, oracle, monkeypatch):
