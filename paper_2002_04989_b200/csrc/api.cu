@@ -308,9 +308,9 @@ int nccl_fail(eigenid_gpu_err* err, ncclResult_t r, const char* where) {
 // Per-stage device timing of run_large: enabled per context through
 // eigenid_gpu_set_profiling (bench.py reads it to time the stage-1 kernel on
 // its own stream) or EIGENID_PROFILE=1 (also printed to stderr).
-// Same-box A/B: the wide stage-1 layout wins at n = 4096, the
-// narrow one at n = 1024.
-constexpr int kStage1WideMinN = 3072;
+// Same-box A/B: narrow wins at n = 1024 (89 ms vs 107 ms for the
+// 1023 minors), widesp at n = 2048 (1127 vs 1161 ms) and n = 4096.
+constexpr int kStage1WideMinN = 2048;
 #ifndef EIGENID_STAGE1_LARGE_LAYOUT
 #define EIGENID_STAGE1_LARGE_LAYOUT kWideSp
 #endif

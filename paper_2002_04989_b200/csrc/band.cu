@@ -30,12 +30,15 @@ namespace eigenid_b200 {
 namespace EIGENID_STAGE1_NS {
 
 constexpr int kB = 32;      // bandwidth / panel width
-// Two layouts, both compiled (namespaces wide / narrow; api.cu picks by n):
-// "wide": 16 warps and one CTA per SM (128-row blocks: half the Bop / VT / X
-// re-reads per trailing element, half the workspace slots), or "narrow": 8 warps and two CTAs per SM (64-row
-// blocks; the second CTA fills the DMMA pipe during the other's panel
-// phases, which weigh more at small n).  Same-box A/B: wide 0.6 % faster at
-// n = 4096 (-23 % DRAM bytes), narrow 13 % faster at n = 1024.
+// Four layouts of this file are compiled (namespaces narrow / wide / wide8 /
+// widesp; api.cu picks narrow below n = 2048 and widesp from there, the other
+// two stay selectable through EIGENID_STAGE1_LAYOUT for A/B runs):
+//   narrow  8 warps, two CTAs per SM, 64-row fused blocks: the second CTA
+//           fills the DMMA pipe during the other's panel phases, which weigh
+//           more at small n (17 % faster than the wide layouts at n = 1024);
+//   wide    16 warps, one CTA per SM, 128-row blocks: half the Bop / VT / X
+//           re-reads per trailing element, half the workspace slots;
+//   wide8, widesp: see EIGENID_STAGE1_RW and EIGENID_STAGE1_SP below.
 #ifndef EIGENID_STAGE1_WIDE
 #define EIGENID_STAGE1_WIDE 1
 #endif
@@ -98,8 +101,8 @@ constexpr int kGramPart = 8 * kSmallMat;             // 8 partial Gram slots
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int kG1S = 3;                             // GEMM 1 cp.async stages
 constexpr int kG2S = 3;                             // GEMM 2 cp.async stages
-// Fused-pass cp.async stages: two in both layouts (a third stage in the wide
-// layout measured 1.1 % slower at n = 4096: 58 KB less L1).
+// Fused-pass cp.async stages: two in every layout (a third stage measured
+// 0.7 % faster in wide, 4 % slower in widesp at n = 4096: 58 KB less L1).
 #ifndef EIGENID_FUSED_STAGES
 #define EIGENID_FUSED_STAGES 2
 #endif

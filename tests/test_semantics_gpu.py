@@ -301,8 +301,9 @@ def test_repeat_runs_are_bit_identical(engine, n, rows):
     """The reference's determinism contract (bit-identical across worker
     counts, test_identity.cpp:130-143) on the device: repeated calls give the
     same bits whatever the solve -> CTA / workspace-slot assignment of the
-    work queues, in both stage-1 layouts (narrow below n = 3072, wide
-    above) and with lambda(A) on the side stream."""
+    work queues, in the default stage-1 layouts (narrow below n = 2048, the
+    warp-specialised widesp layout from there) and with lambda(A) on the side
+    stream."""
     import paper_2002_04989_b200 as eid
     a = eid.random_symmetric(7, n) * np.sqrt(2.0 / n)
     ref = engine.minor_spectra(a, 0, rows)
