@@ -49,7 +49,9 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 P_FP64_MEASURED_TFLOPS = 37.09   # tools/fp64_peak.cu DMMA m8n8k4 on this pool
 P_FP64_SOURCE = ("measured: tools/fp64_peak.cu, DMMA m8n8k4 f64 "
-                 "(profiles/r01_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)")
+                 "(profiles/r01_fp64_peak.json, re-measured in round 2: 37.01 burst / "
+                 "37.08 sustained at 1965 MHz, profiles/r02_fp64_peak.json; "
+                 "MEASURED_PEAKS.json has no FP64 entry)")
 METRIC = "|v_ij|^2 components/sec"
 UNIT = "components/s"
 SUB_STEPS = {"C1": 20, "C2": 10, "C3": 5, "C4": 2, "C5": 2}
@@ -652,7 +654,7 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
         # launch's solve count
         traffic = (1.012767e12 + 0.616259e12) / 147 * (rows + 1) if n == 4096 else None
         line["roofline"] = {
-            "bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA)",
+            "bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA; widesp layout)",
             "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / P_FP64_MEASURED_TFLOPS, "traffic": traffic,
             "traffic_note": "ncu dram__bytes_read+write per solve x solves",
