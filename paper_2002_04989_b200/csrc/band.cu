@@ -936,6 +936,19 @@ __device__ __forceinline__ void mbar_inval(unsigned long long* bar) {
 #endif
 static_assert(!EIGENID_PIPE_MBAR || EIGENID_SPLIT_BAR, "pipe");
 
+// Row blocks of the fused pass are aligned to the END of the trailing matrix
+// (rounded up to a whole 32-column tile, so block starts stay multiples of 32
+// and a row block still crosses the diagonal in four tiles): the short block
+// is the FIRST one (rows fused_rb0 .. < 0 do not exist and are zero-filled /
+// skipped through row_ok), where it costs the few tiles up to the diagonal,
+// instead of the last one, where it would cost a full row of tiles (on average
+// 49 of 128 rows idle: 3.5 % of the DMMAs at n = 4096).
+__device__ __forceinline__ int fused_rb0(int sn) {
+  const int end = (sn + kG2N - 1) / kG2N * kG2N;
+  return -((kG2M - end % kG2M) % kG2M);
+}
+__device__ __forceinline__ bool row_ok(int r, int sn) { return (unsigned)r < (unsigned)sn; }
+
 #if !EIGENID_STAGE1_SP
 __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                            const double* Vp, const double* VTn, double* Xn,
@@ -967,7 +980,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
   if (tid == 0) mbar_init(cbar, kNW);
   __syncthreads();
 #endif
-  for (int rb = 0; rb < sn; rb += kG2M) {
+  for (int rb = fused_rb0(sn); rb < sn; rb += kG2M) {
     double2 af[kRW][kG2K / 8];
 #pragma unroll
     for (int mt = 0; mt < kRW; ++mt) {
@@ -976,7 +989,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       for (int q = 0; q < kG2K / 8; ++q) {
         const int k = 8 * q + 2 * kk;
         double2 v = make_double2(0.0, 0.0);
-        if (r < sn)
+        if (row_ok(r, sn))
           v = *reinterpret_cast<const double2*>(k < kB ? W2p + (long long)r * kB + k
                                                        : Vp + (long long)r * kB + (k - kB));
         af[mt][q] = make_double2(-v.x, -v.y);
@@ -996,7 +1009,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
           const int row = t >> 5, k2 = (t & 31) * 2;
           const int gr = cb + row;
-          const int bytes = gr < sn ? 16 : 0;
+          const int bytes = row_ok(gr, sn) ? 16 : 0;
           const long long g = (long long)(bytes ? gr : 0) * kB;
           const double* src = k2 < kB ? Vp + g + k2 : W2p + g + (k2 - kB);
           cp_async16(st + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
@@ -1006,7 +1019,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           const int row = t >> 4, c2 = (t & 15) * 2;
           const int gr = rb + row, gc = cb + c2;
           int bytes = 0;
-          if (gr < sn && gc < sn) bytes = gc + 1 < sn ? 16 : 8;
+          if (row_ok(gr, sn) && gc < sn) bytes = gc + 1 < sn ? 16 : 8;
           cp_async16(cs + cswz(row, c2), bytes ? A22n + (long long)gr * ldw + gc : A22n,
                      bytes);
         }
@@ -1014,7 +1027,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         for (int t = tid; t < kB * (kB / 2); t += kNT) {
           const int row = t >> 4, c2 = (t & 15) * 2;
           const int gr = cb + row;
-          const int bytes = gr < sn ? 16 : 0;
+          const int bytes = row_ok(gr, sn) ? 16 : 0;
           cp_async16(vc + row * kFVLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
                      bytes);
         }
@@ -1031,7 +1044,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     // fixed offsets from three pointers that advance by one tile, so a stage
     // is a handful of unpredicated cp.async off immediate offsets instead of
     // ~230 instructions of index and predicate arithmetic.
-    const bool interior = rb + kG2M <= sn;
+    const bool interior = rb >= 0 && rb + kG2M <= sn;
     auto stage_fast = [&](int ci) {
       if (ci < ncb) {
         constexpr int kBopIt = kG2N * (kG2K / 2) / kNT, kBopRows = kNT / 32;
@@ -1070,7 +1083,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     for (int t = tid; t < kG2M * (kB / 2); t += kNT) {
       const int row = t >> 4, c2 = (t & 15) * 2;
       const int gr = rb + row;
-      const int bytes = gr < sn ? 16 : 0;
+      const int bytes = row_ok(gr, sn) ? 16 : 0;
       cp_async16(sVr + row * kFVRLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
                  bytes);
     }
@@ -1236,7 +1249,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
           for (int nt = 0; nt < kG2N / 8; ++nt) {
             const int col = cb + 8 * nt + 2 * kk;
-            if (r < sn) {
+            if (row_ok(r, sn)) {
               double* p = A22n + (long long)r * ldw + col;
               if (col + 1 < sn)
                 *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
@@ -1310,7 +1323,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
     for (int mt = 0; mt < kRW; ++mt) {
       const int r = rb + crow0 + 8 * mt;
-      if (r < sn) {
+      if (row_ok(r, sn)) {
 #pragma unroll
         for (int nt = 0; nt < kG2N / 8; ++nt) {
           double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + 8 * nt + 2 * kk);
@@ -1395,10 +1408,10 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     const int pt = tid - 32 * kCW;
     int g = 0;
     unsigned ebits = 0, rbpar = 0;
-    for (int rb = 0; rb < sn; rb += kG2M) {
+    for (int rb = fused_rb0(sn); rb < sn; rb += kG2M) {
       const int cend = min(rb + kG2M, sn);
       const int ncb = (cend + kG2N - 1) / kG2N;
-      const bool interior = rb + kG2M <= sn;
+      const bool interior = rb >= 0 && rb + kG2M <= sn;
       for (int ci = 0; ci < ncb; ++ci, ++g) {
         const int sb = g % kFS;
         if (g >= kFS) {
@@ -1444,7 +1457,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           for (int t = pt; t < kG2N * (kG2K / 2); t += kPT) {
             const int row = t >> 5, k2 = (t & 31) * 2;
             const int gr = cb + row;
-            const int bytes = gr < sn ? 16 : 0;
+            const int bytes = row_ok(gr, sn) ? 16 : 0;
             const long long gg = (long long)(bytes ? gr : 0) * kB;
             const double* src = k2 < kB ? Vp + gg + k2 : W2p + gg + (k2 - kB);
             cp_async16(st + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
@@ -1454,7 +1467,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
             const int row = t >> 4, c2 = (t & 15) * 2;
             const int gr = rb + row, gc = cb + c2;
             int bytes = 0;
-            if (gr < sn && gc < sn) bytes = gc + 1 < sn ? 16 : 8;
+            if (row_ok(gr, sn) && gc < sn) bytes = gc + 1 < sn ? 16 : 8;
             cp_async16(cs + cswz(row, c2), bytes ? A22n + (long long)gr * ldw + gc : A22n,
                        bytes);
           }
@@ -1462,7 +1475,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           for (int t = pt; t < kB * (kB / 2); t += kPT) {
             const int row = t >> 4, c2 = (t & 15) * 2;
             const int gr = cb + row;
-            const int bytes = gr < sn ? 16 : 0;
+            const int bytes = row_ok(gr, sn) ? 16 : 0;
             cp_async16(vc + row * kFVLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
                        bytes);
           }
@@ -1471,14 +1484,14 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         if (ci == 0) {
           // VTn[rb] rows: the compute warps must be done with the previous
           // row block's transposed products
-          if (rb > 0) {
+          if (rb != fused_rb0(sn)) {
             mbar_wait(rbdone, rbpar);
             rbpar ^= 1u;
           }
           for (int t = pt; t < kG2M * (kB / 2); t += kPT) {
             const int row = t >> 4, c2 = (t & 15) * 2;
             const int gr = rb + row;
-            const int bytes = gr < sn ? 16 : 0;
+            const int bytes = row_ok(gr, sn) ? 16 : 0;
             cp_async16(sVr + row * kFVRLD + c2, VTn + (long long)(bytes ? gr : 0) * kB + c2,
                        bytes);
           }
@@ -1499,7 +1512,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     for (int mt = 0; mt < kRW; ++mt) crow[mt] = 8 * (warp + kCW * mt) + mm;
     int g = 0;
     unsigned fbits = 0, cphase = 0, svphase = 0;
-    for (int rb = 0; rb < sn; rb += kG2M) {
+    for (int rb = fused_rb0(sn); rb < sn; rb += kG2M) {
       double2 af[kRW][kG2K / 8];
 #pragma unroll
       for (int mt = 0; mt < kRW; ++mt) {
@@ -1508,7 +1521,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         for (int q = 0; q < kG2K / 8; ++q) {
           const int k = 8 * q + 2 * kk;
           double2 v = make_double2(0.0, 0.0);
-          if (r < sn)
+          if (row_ok(r, sn))
             v = *reinterpret_cast<const double2*>(k < kB ? W2p + (long long)r * kB + k
                                                          : Vp + (long long)r * kB + (k - kB));
           af[mt][q] = make_double2(-v.x, -v.y);
@@ -1521,7 +1534,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         for (int nt = 0; nt < kG2N / 8; ++nt) xr[mt][nt][0] = xr[mt][nt][1] = 0.0;
       const int cend = min(rb + kG2M, sn);
       const int ncb = (cend + kG2N - 1) / kG2N;
-      const bool interior = rb + kG2M <= sn;
+      const bool interior = rb >= 0 && rb + kG2M <= sn;
       double x2n[kXT][2];
       auto load_x2 = [&](int ci) {
         const int xr0 = ci * kG2N + 8 * (warp / (4 / kXT)) + mm;
@@ -1572,13 +1585,13 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         // or wholly past the last row skips its update and row product
         // (exact zeros), and the transposed product runs over the contraction
         // rows [d, rows in range) only.
-        const int dskip = (EIGENID_SP_SKIP && diag) ? max(cb - rb, 0) : 0;
+        const int dskip = (EIGENID_SP_SKIP && EIGENID_SP_SKIP != 3 && diag) ? max(cb - rb, 0) : 0;
         const int kend4 = (EIGENID_SP_SKIP && diag) ? (min(kG2M, sn - rb) + 3) / 4 : kG2M / 4;
         bool live[kRW];
 #pragma unroll
         for (int mt = 0; mt < kRW; ++mt)
           live[mt] = !(EIGENID_SP_SKIP && diag) ||
-                     (8 * (warp + kCW * mt) + 7 >= dskip && rb + 8 * (warp + kCW * mt) < sn);
+                     (8 * (warp + kCW * mt) + 7 >= dskip && row_ok(rb + 8 * (warp + kCW * mt) + 7, sn));
         // ---- rank-2kB update of this lane's C rows
         double acc[kRW][kG2N / 8][2];
 #pragma unroll
@@ -1665,7 +1678,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
             for (int nt = 0; nt < kG2N / 8; ++nt) {
               const int col = cb + 8 * nt + 2 * kk;
-              if (r < sn) {
+              if (row_ok(r, sn)) {
                 double* p = A22n + (long long)r * ldw + col;
                 if (col + 1 < sn)
                   *reinterpret_cast<double2*>(p) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
@@ -1709,7 +1722,9 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         ++g;
       };
       for (int ci = 0; ci < ncb; ++ci) {
-        if (ci * kG2N + kB > rb || (EIGENID_SP_SKIP && !interior))
+        // EIGENID_SP_SKIP: 1 = diagonal and tail tiles, 2 = diagonal tiles
+        // only, 3 = tail row blocks only (timing experiments)
+        if (ci * kG2N + kB > rb || ((EIGENID_SP_SKIP & 1) && !interior))
           tile(ci, std::true_type{});
         else
           tile(ci, std::false_type{});
@@ -1723,7 +1738,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
       for (int mt = 0; mt < kRW; ++mt) {
         const int r = rb + crow[mt];
-        if (r < sn) {
+        if (row_ok(r, sn)) {
 #pragma unroll
           for (int nt = 0; nt < kG2N / 8; ++nt) {
             double2* p = reinterpret_cast<double2*>(Xn + (long long)r * kB + 8 * nt + 2 * kk);
