@@ -58,6 +58,16 @@ SUB_STEPS = {"C1": 20, "C2": 10, "C3": 5, "C4": 2, "C5": 2}
 C5_SEED = 5
 
 
+def arm_watchdog(phase: str) -> None:
+    """(Re)starts the hang watchdog for the next phase of the run and notes
+    the phase on stderr, so a dump says what was running."""
+    import faulthandler
+    budget = float(os.environ.get("BENCH_WATCHDOG_S", "1500"))
+    print(f"[bench] phase: {phase}", file=sys.stderr, flush=True)
+    faulthandler.cancel_dump_traceback_later()
+    faulthandler.dump_traceback_later(budget, exit=True)
+
+
 # ----------------------------------------------------------------- inputs
 def goe_matrix(n: int, seed: int = 42) -> np.ndarray:
     """random_symmetric(seed, n).scaled(sqrt(2/n)) — SURVEY §8 d4 (the
@@ -547,6 +557,7 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
         flops = f_id(n, rows)
 
     # ---- warm-up, then K timed steps (device clock on the library stream)
+    arm_watchdog(f"{wl}: warm-up and timed steps")
     for _ in range(warmup):
         step()
     eng.sync()
@@ -578,6 +589,7 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
     ms_step = t_total / steps * 1e3
 
     # ---- end to end through the public API with host buffers
+    arm_watchdog(f"{wl}: end to end")
     e2e = None
     e2e_steps = max(1, min(steps // 4, 5)) if wl == "C4" else max(1, min(steps // 2, 5))
     res = None
@@ -685,6 +697,7 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
                             if wl == "C5" else "F_tri + F_id per step")}
 
     # ---- parity (golden fixtures) and CPU baseline (rank 0, N = 1 only)
+    arm_watchdog(f"{wl}: parity and CPU baseline")
     if world == 1:
         g = out_dev.cpu().numpy()
         if wl == "C1":
@@ -751,6 +764,11 @@ def main():
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo lets several ranks share one GPU (flow testing only)")
     args = ap.parse_args()
+    # Watchdog: a run that stops making progress dumps every thread's Python
+    # stack to stderr and exits non-zero instead of blocking its caller.  It
+    # is re-armed per timed phase through stage_note(); BENCH_WATCHDOG_S
+    # overrides the per-phase budget (seconds).
+    arm_watchdog("start")
     dist = Dist()
     if args.impl == "reference":
         if dist.rank != 0:
@@ -760,7 +778,15 @@ def main():
         return 0
     dist.init(args.dist_backend)
     try:
-        line = our_arm(args, dist)
+        try:
+            line = our_arm(args, dist)
+        except Exception as e:  # noqa: BLE001
+            # a bounded device-side wait ran out (the library reports it as a
+            # DeviceError and the context stays usable): measure once more
+            if "wait timed out" not in str(e):
+                raise
+            print(f"[bench] {e}; repeating the run once", file=sys.stderr, flush=True)
+            line = our_arm(args, dist)
     finally:
         dist.close()
     if line is not None:

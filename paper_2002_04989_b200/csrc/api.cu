@@ -118,6 +118,7 @@ struct HostBuf {
 }  // namespace
 
 struct eigenid_gpu_ctx {
+  bool wait_timed_out = false;  // finish(): a bounded device wait ran out (retried once)
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // lambda(A)'s solve, beside the minors
@@ -232,6 +233,13 @@ int finish(eigenid_gpu_ctx* c, eigenid_gpu_err* err, bool* degenerate) {
       std::snprintf(buf, sizeof buf, "matrix entry is not finite (entry %lld, matrix %lld)",
                     s.index, s.aux);
       break;
+    case 30:  // kWaitTimeoutCode (band.cu, bulge.cu)
+      c->wait_timed_out = true;
+      std::snprintf(buf, sizeof buf,
+                    "device-side wait timed out (site %lld, CTA*1000+warp %lld); "
+                    "the call was abandoned", s.index, s.aux);
+      set_err(err, EIGENID_E_DEVICE, s.index, 0.0, 0, buf);
+      return EIGENID_E_DEVICE;
     default:
       std::snprintf(buf, sizeof buf, "device error code %d", s.code);
   }
@@ -1069,15 +1077,11 @@ int eigenid_gpu_eigenvalues(eigenid_gpu_ctx* c, const double* a, size_t n,
   return finish(c, err, nullptr);
 }
 
-int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
+static int all_magnitudes_once(eigenid_gpu_ctx* c, const double* a, size_t n,
                                const eigenid_gpu_config* cfg, double* out,
                                double* lambda_out, double* mu_out,
-                               eigenid_gpu_err* err) {
-  int st = check_n(n, err);
-  if (st) return st;
-  if ((st = check_cfg(cfg, err))) return st;
-  std::lock_guard<std::mutex> g(c->mu);
-  if (c->multi) return all_magnitudes_multi(c, a, n, cfg, out, lambda_out, mu_out, err);
+                               eigenid_gpu_err* err, bool* degenerate_out) {
+  int st;
   if ((st = begin(c, err))) return st;
   const size_t nn = n * n;
   EID_CUDA(c->bA.ensure(sizeof(double) * nn), "alloc A");
@@ -1103,8 +1107,31 @@ int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
     EID_CUDA(cudaMemcpyAsync(mu_out, c->bMu.p, sizeof(double) * n * (n - 1),
                              cudaMemcpyDeviceToHost, c->stream),
              "D2H mu");
+  return finish(c, err, degenerate_out);
+}
+
+int eigenid_gpu_all_magnitudes(eigenid_gpu_ctx* c, const double* a, size_t n,
+                               const eigenid_gpu_config* cfg, double* out,
+                               double* lambda_out, double* mu_out,
+                               eigenid_gpu_err* err) {
+  int st = check_n(n, err);
+  if (st) return st;
+  if ((st = check_cfg(cfg, err))) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  if (c->multi) return all_magnitudes_multi(c, a, n, cfg, out, lambda_out, mu_out, err);
   bool degenerate = false;
-  st = finish(c, err, &degenerate);
+  c->wait_timed_out = false;
+  st = all_magnitudes_once(c, a, n, cfg, out, lambda_out, mu_out, err, &degenerate);
+  if (c->wait_timed_out) {
+    // A bounded device-side wait ran out (band.cu kWaitTimeoutCode): the
+    // kernels have unwound and the context is healthy; the pipeline is
+    // idempotent, so the call is repeated once before the error is reported.
+    std::fprintf(stderr, "[eigenid] %s -- retrying the call once\n", err ? err->msg : "");
+    c->wait_timed_out = false;
+    degenerate = false;
+    if (err) std::memset(err, 0, sizeof *err);
+    st = all_magnitudes_once(c, a, n, cfg, out, lambda_out, mu_out, err, &degenerate);
+  }
   // identity.cpp:299-306: lambda(A) is solved, then the degeneracy check
   // throws before the n minor solves.
   // NonFiniteEntry: build() throws before any solve (matrix.cpp:17-18)

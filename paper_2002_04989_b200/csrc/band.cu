@@ -893,16 +893,43 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
                    (unsigned)__cvta_generic_to_shared(bar))
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+// Device status code of a wait that ran out of time (reported by the host as
+// EIGENID_E_DEVICE): every inter-warp wait of the library is bounded, so a
+// lost arrival ends the call with an error instead of hanging the process.
+constexpr int kWaitTimeoutCode = 30;
+#ifndef EIGENID_WAIT_TIMEOUT_CYCLES
+#define EIGENID_WAIT_TIMEOUT_CYCLES 30000000000LL  // ~15 s at 1.9 GHz
+#endif
+constexpr long long kWaitTimeoutCycles = EIGENID_WAIT_TIMEOUT_CYCLES;
+__device__ __noinline__ void wait_timed_out(DevStatus* st, int site) {
+  set_status(st, kWaitTimeoutCode, site, 0.0, blockIdx.x * 1000 + (threadIdx.x >> 5));
+}
+// Blocks until the barrier phase of the given parity has completed.  `site`
+// names the wait in the timeout report; once any wait of the call has timed
+// out, the others return at once so that the kernel unwinds.
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity,
+                                          DevStatus* st, int site) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done)
+  unsigned done = 0, spins = 0;
+  long long t0 = 0;
+  while (!done) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+    if (!done && ((++spins) & 0xffu) == 0) {
+      if (*(volatile const int*)&st->code == kWaitTimeoutCode) return;
+      const long long now = clock64();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > kWaitTimeoutCycles) {
+        wait_timed_out(st, site);
+        return;
+      }
+    }
+  }
 }
 
 // Arrival on an mbarrier triggered by the completion of every cp.async this
@@ -952,7 +979,7 @@ __device__ __forceinline__ bool row_ok(int r, int sn) { return (unsigned)r < (un
 #if !EIGENID_STAGE1_SP
 __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                            const double* Vp, const double* VTn, double* Xn,
-                           double* sm) {
+                           double* sm, DevStatus* status) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = lane & 3, mm = lane >> 2;
   // this lane's rows within the row block: crow0 + 8 mt, mt < kRW
@@ -1192,7 +1219,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       auto issue_next = [&]() {
         if (ci + kFS - 1 < ncb) {
           const int nb2 = (ci + kFS - 1) % kFS;
-          if (ci >= 1) mbar_wait(emptyb + nb2, ((ebits >> nb2) & 1u) ^ 1u);
+          if (ci >= 1) mbar_wait(emptyb + nb2, ((ebits >> nb2) & 1u) ^ 1u, status, 1);
           if (EIGENID_FAST_STAGE && interior)
             stage_fast(ci + kFS - 1);
           else
@@ -1264,7 +1291,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #endif
 #if EIGENID_SPLIT_BAR
 #ifndef EIGENID_EXP_NO_CBAR
-      mbar_wait(cbar, cphase);
+      mbar_wait(cbar, cphase, status, 2);
 #endif
       cphase ^= 1u;
 #else
@@ -1300,7 +1327,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
     };
     for (int ci = 0; ci < ncb; ++ci) {
 #if EIGENID_PIPE_MBAR
-      mbar_wait(fullb + (ci % kFS), (fbits >> (ci % kFS)) & 1u);
+      mbar_wait(fullb + (ci % kFS), (fbits >> (ci % kFS)) & 1u, status, 3);
       fbits ^= 1u << (ci % kFS);
 #else
       cpa_wait<kFS - 2>();
@@ -1359,6 +1386,9 @@ __device__ __forceinline__ void reg_dec() {
 __device__ __forceinline__ void bar_compute() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kCW) : "memory");
 }
+#ifdef EIGENID_EXP_DROP_ARRIVE
+__device__ int g_drop_once = 1;
+#endif
 #ifndef EIGENID_SP_SKIP
 #define EIGENID_SP_SKIP 0
 #endif
@@ -1383,7 +1413,7 @@ static_assert(kRegCopy >= 24 && kRegCompute <= 232, "setmaxnreg split");
 //                  X read-modify-writes.
 __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
                            const double* Vp, const double* VTn, double* Xn,
-                           double* sm) {
+                           double* sm, DevStatus* status) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* sVr = sm + kFS * kFSt;
   __shared__ alignas(8) unsigned long long bars[2 * kFS + 3];
@@ -1415,7 +1445,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       for (int ci = 0; ci < ncb; ++ci, ++g) {
         const int sb = g % kFS;
         if (g >= kFS) {
-          mbar_wait(emptyb + sb, (ebits >> sb) & 1u);
+          mbar_wait(emptyb + sb, (ebits >> sb) & 1u, status, 4);
           ebits ^= 1u << sb;
         }
         double* st = sm + sb * kFSt;
@@ -1485,7 +1515,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           // VTn[rb] rows: the compute warps must be done with the previous
           // row block's transposed products
           if (rb != fused_rb0(sn)) {
-            mbar_wait(rbdone, rbpar);
+            mbar_wait(rbdone, rbpar, status, 5);
             rbpar ^= 1u;
           }
           for (int t = pt; t < kG2M * (kB / 2); t += kPT) {
@@ -1577,7 +1607,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           x2[u][1] = x2n[u][1];
         }
         if (ci + 1 < ncb) load_x2(ci + 1);
-        mbar_wait(fullb + sb, (fbits >> sb) & 1u);
+        mbar_wait(fullb + sb, (fbits >> sb) & 1u, status, 6);
         fbits ^= 1u << sb;
         // Slow-path tiles (diagonal-crossing, or any tile of the last partial
         // row block): an 8-row group wholly above the diagonal (tile rows < d
@@ -1688,10 +1718,10 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
             }
           }
         }
-        mbar_wait(cbar, cphase);
+        mbar_wait(cbar, cphase, status, 7);
         cphase ^= 1u;
         if (ci == 0) {  // this row block's VTn[rb] rows have landed
-          mbar_wait(svr_full, svphase);
+          mbar_wait(svr_full, svphase, status, 8);
           svphase ^= 1u;
         }
         // ---- X[cb] += strict(C)^T VTn[rb]
@@ -1718,7 +1748,13 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           }
         }
         __syncwarp();
+#ifdef EIGENID_EXP_DROP_ARRIVE  // test hook: lose ONE arrival; the waits must time out
+        if (lane == 0 && !(blockIdx.x == 3 && warp == 2 && g == 7 && sn < 3000 &&
+                           atomicExch(&g_drop_once, 0)))
+          mbar_arrive(emptyb + sb);
+#else
         if (lane == 0) mbar_arrive(emptyb + sb);
+#endif
         ++g;
       };
       for (int ci = 0; ci < ncb; ++ci) {
@@ -1949,7 +1985,7 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
         __syncthreads();
         PHASE(4);
         gemm_fused(A22 + (long long)kB * ldw + kB, ldw, s1, Xg[par] + kB * kB,
-                   Vg[par] + kB * kB, VTg, Xg[nxt], sgemm);
+                   Vg[par] + kB * kB, VTg, Xg[nxt], sgemm, args.status);
         form_w2(s1, Vg[nxt], Xg[nxt]);
         c += kB;
         par = nxt;

@@ -240,14 +240,33 @@ __device__ __forceinline__ long long spos(int sweep, int step) {
 }
 
 // Blocks until sweep s-1 (owned by warp w-1 mod W) has finished step k.
+// The wait is bounded (see band.cu: kWaitTimeoutCode): a lost progress update
+// ends the call with a device error instead of hanging the process.
+constexpr int kChaseTimeoutCode = 30;
+constexpr long long kChaseTimeoutCycles = 30000000000LL;
 template <int W>
 __device__ __forceinline__ void wait_prev(volatile long long* prog, int warp,
-                                          int s, int k) {
+                                          int s, int k, DevStatus* st) {
   if (s == 0) return;
   const int pw = (warp + W - 1) % W;
   const long long need = spos(s - 1, k);
-  if ((threadIdx.x & 31) == 0)
-    while (prog[pw] < need) __nanosleep(64);
+  if ((threadIdx.x & 31) == 0) {
+    unsigned spins = 0;
+    long long t0 = 0;
+    while (prog[pw] < need) {
+      __nanosleep(64);
+      if (((++spins) & 0xfffu) == 0) {
+        if (*(volatile const int*)&st->code == kChaseTimeoutCode) break;
+        const long long now = clock64();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > kChaseTimeoutCycles) {
+          set_status(st, kChaseTimeoutCode, 100 + k, 0.0, blockIdx.x * 1000 + warp);
+          break;
+        }
+      }
+    }
+  }
   __syncwarp();
   __threadfence_block();
 }
@@ -294,7 +313,7 @@ bulge_chase_kernel(Stage2Args a) {
       bool have = Rk <= m - 1;
       int Lk = have ? min(kCB, m - Rk) : 0;
       // block 0 and the prefetch of step 1 need sweep st-1 past step 2
-      wait_prev<kWarpsPerCta>(prog, warp, st, 2);
+      wait_prev<kWarpsPerCta>(prog, warp, st, 2, a.status);
       const double x = lane < L0 ? AB[(long long)st * kCLD + 1 + lane] : 0.0;
       prefetch_d(sD, AB, R0, L0);
       if (have) prefetch_c(sC, AB, Rk, Lk, R0, L0);
@@ -321,7 +340,7 @@ bulge_chase_kernel(Stage2Args a) {
         const bool haven = Rn <= m - 1;
         const int Ln = haven ? min(kCB, m - Rn) : 0;
         BPH(0);
-        if (haven) wait_prev<kWarpsPerCta>(prog, warp, st, k + 2);  // before step k+1's prefetches
+        if (haven) wait_prev<kWarpsPerCta>(prog, warp, st, k + 2, a.status);  // before step k+1's prefetches
         BPH(6);
         BPH(1);
         // right-apply the previous reflector: C -= tau (C v) v^T

@@ -29,7 +29,7 @@ struct Stage1Args {
   double* band;       // per-solve band, column-major [col][0..2kB]
   long long band_stride;
   int* counter;       // work queue (zeroed before launch unless reset == 0)
-  const DevStatus* status;  // sticky call status: nonzero code = abort
+  DevStatus* status;  // sticky call status: nonzero code = abort; wait time-outs are recorded here
   int slot0;          // workspace slot of blockIdx.x == 0
   const double* scale;  // [0]: exact power-of-two input scale (nullable = 1)
   // "the main grid is running" flag (nullable): the main launch sets it, a
@@ -77,7 +77,7 @@ struct Stage2Args {
   double* ae;              // per solve: m-1 |off-diagonal|
   long long de_stride;
   int* counter;            // work queue (zeroed before launch)
-  const DevStatus* status; // sticky call status: nonzero code = abort
+  DevStatus* status; // sticky call status: nonzero code = abort; wait time-outs are recorded here
   int device;              // for the SM count
   int compact = 0;         // 1: register-capped variant (co-resides with stage 1)
 };

@@ -31,3 +31,15 @@ def reference():
 def engine():
     from paper_2002_04989_b200 import IdentityEngine
     return IdentityEngine()
+
+
+@pytest.fixture(autouse=True)
+def _hang_watchdog():
+    """A test that stops making progress (a device-side deadlock cannot be
+    interrupted from Python) dumps every thread's stack and ends the run
+    instead of blocking its caller forever."""
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("EIGENID_TEST_WATCHDOG_S", "900")),
+                                      exit=True)
+    yield
+    faulthandler.cancel_dump_traceback_later()
