@@ -863,6 +863,82 @@ __device__ void gemm2(double* A22, int ldw, int s, const double* W2,
   __syncthreads();
 }
 
+// ---- next panel's columns: A22[:, 0:kB] -= (W2 V^T + V W2^T)[:, 0:kB] -------
+// The one-tile-per-row-block case of GEMM 2 (same arithmetic, element by
+// element), restructured for latency: the 32 Bop rows are staged once, then
+// every warp streams its own 8-row groups — A-operand rows and C rows straight
+// from global memory into registers, the next group's loads in flight while
+// the current one runs its 64 DMMAs — with no CTA barrier per row block (GEMM 2
+// spent ~2 us per 128 rows waiting for a cp.async round trip: 9.6 ms per solve
+// at n = 4096).
+__device__ void update_cols(double* A22, int ldw, int s, const double* W2, const double* V,
+                            double* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = lane & 3, mm = lane >> 2;
+  __syncthreads();
+  for (int t = tid; t < kG2N * (kG2K / 2); t += kNT) {
+    const int row = t >> 5, k2 = (t & 31) * 2;
+    const int bytes = row < s ? 16 : 0;
+    const long long g = (long long)(bytes ? row : 0) * kB;
+    const double* src = k2 < kB ? V + g + k2 : W2 + g + (k2 - kB);
+    cp_async16(sm + row * kG2K + (k2 ^ (8 * (row & 1))), src, bytes);
+  }
+  cpa_commit();
+  struct Group {
+    double2 af[kG2K / 8];
+    double2 c[kG2N / 8];
+  };
+  auto load = [&](int r, Group& g) {
+#pragma unroll
+    for (int q = 0; q < kG2K / 8; ++q) {
+      const int k = 8 * q + 2 * kk;
+      double2 v = make_double2(0.0, 0.0);
+      if (r < s)
+        v = *reinterpret_cast<const double2*>(k < kB ? W2 + (long long)r * kB + k
+                                                     : V + (long long)r * kB + (k - kB));
+      g.af[q] = make_double2(-v.x, -v.y);
+    }
+#pragma unroll
+    for (int nt = 0; nt < kG2N / 8; ++nt)
+      g.c[nt] = r < s ? *reinterpret_cast<const double2*>(A22 + (long long)r * ldw + 8 * nt + 2 * kk)
+                      : make_double2(0.0, 0.0);
+  };
+  Group cur, nxt;
+  int r = 8 * warp + mm;
+  load(r, cur);
+  cpa_wait0();
+  __syncthreads();
+  for (; r - mm < s; r += 8 * kNW) {
+    load(r + 8 * kNW, nxt);  // rows past the end load nothing
+    double acc[kG2N / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < kG2N / 8; ++nt) {
+      acc[nt][0] = cur.c[nt].x;
+      acc[nt][1] = cur.c[nt].y;
+    }
+#pragma unroll
+    for (int q = 0; q < kG2K / 8; ++q) {
+      const int kl = (8 * q + 2 * kk) ^ (8 * (mm & 1));
+      double2 bf[kG2N / 8];
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt)
+        bf[nt] = *reinterpret_cast<const double2*>(sm + (8 * nt + mm) * kG2K + kl);
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], cur.af[q].x, bf[nt].x);
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt) dmma(acc[nt][0], acc[nt][1], cur.af[q].y, bf[nt].y);
+    }
+    if (r < s) {
+#pragma unroll
+      for (int nt = 0; nt < kG2N / 8; ++nt)
+        *reinterpret_cast<double2*>(A22 + (long long)r * ldw + 8 * nt + 2 * kk) =
+            make_double2(acc[nt][0], acc[nt][1]);
+    }
+    cur = nxt;
+  }
+  __syncthreads();
+}
+
 // ---- fused: rest of panel p's update + SYMM of panel p+1 -----------------
 // A22n is the trailing matrix of panel p+1 (A22 of panel p without its first
 // kB rows and columns, whose update was applied beforehand).  One pass over
@@ -1978,7 +2054,11 @@ __global__ void __launch_bounds__(kNT, kCtasPerSm) band_reduce_kernel(Stage1Args
           c += kB;
           break;
         }
-        gemm2(A22, ldw, s, Xg[par], Vg[par], sgemm, 1);        // next panel's columns
+#ifndef EIGENID_OLD_UPDATE_COLS
+        update_cols(A22, ldw, s, Xg[par], Vg[par], sgemm);     // next panel's columns
+#else
+        gemm2(A22, ldw, s, Xg[par], Vg[par], sgemm, 1);
+#endif
         const int nxt = par ^ 1;
         factor(c + kB, s1, Vg[nxt], Xg[nxt]);
         for (int t = tid; t < s1 * kB; t += kNT) Xg[nxt][t] = 0.0;
