@@ -140,6 +140,15 @@ constexpr int kRed = kNW + kNW * kB;
 constexpr int kStage1SmemDoubles = kGemmSmem + 3 * kSmallMat + kRed + 4 * kB;
 static_assert(kGemmSmem >= kGramPart && kGemmSmem >= 2 * kSmallMat, "smem");
 
+// unroll factors of the streaming panel passes (loads in flight per warp)
+#ifndef EIGENID_GRAM_UNROLL
+#define EIGENID_GRAM_UNROLL 2
+#endif
+#ifndef EIGENID_RT_UNROLL
+#define EIGENID_RT_UNROLL 2
+#endif
+constexpr int kGramUnroll = EIGENID_GRAM_UNROLL, kRtUnroll = EIGENID_RT_UNROLL;
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile(
       "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, "
@@ -283,7 +292,7 @@ __device__ void gram(const double* L, int ldl, const double* R, int ldr, int s,
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 2
+#pragma unroll kGramUnroll
   for (int i = warp; 4 * i < s; i += kNT / 32) {
     const int r = 4 * i + kk;
     double a[4], b[4];
@@ -348,7 +357,7 @@ __device__ void row_transform(const double* L, int ldl, const double* Mt,
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 2
+#pragma unroll kRtUnroll
     for (int k4 = 0; k4 < kB / 4; ++k4) {
       const int k = 4 * k4 + kk;
       double af[4], bf[4];
