@@ -1474,6 +1474,9 @@ __device__ __forceinline__ void bar_compute() {
 #ifdef EIGENID_EXP_DROP_ARRIVE
 __device__ int g_drop_once = 1;
 #endif
+#ifndef EIGENID_SP_SKIP0
+#define EIGENID_SP_SKIP0 1
+#endif
 #ifndef EIGENID_SP_SKIP
 #define EIGENID_SP_SKIP 0
 #endif
@@ -1673,8 +1676,15 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         }
       };
       load_x2(0);
-      auto tile = [&](int ci, auto diag_tag) {
+      // skip0: a diagonal tile whose rows 0..63 (every warp's first 8-row
+      // group) lie wholly above the diagonal (d = cb - rb >= 64): that group's
+      // update, row product and write-back are compiled out and the
+      // transposed product starts at contraction row 64 (all exact zeros
+      // otherwise) -- a compile-time variant, no per-tile liveness tests.
+      auto tile = [&](int ci, auto diag_tag, auto skip0_tag) {
         constexpr bool diag = decltype(diag_tag)::value;
+        constexpr bool skip0 = decltype(skip0_tag)::value;
+        static_assert(!skip0 || (diag && kRW == 2 && kG2M == 128), "skip0");
         const int cb = ci * kG2N;
         const int sb = g % kFS;
         const double* b = sm + sb * kFSt;
@@ -1705,12 +1715,15 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         bool live[kRW];
 #pragma unroll
         for (int mt = 0; mt < kRW; ++mt)
-          live[mt] = !(EIGENID_SP_SKIP && diag) ||
-                     (8 * (warp + kCW * mt) + 7 >= dskip && row_ok(rb + 8 * (warp + kCW * mt) + 7, sn));
+          live[mt] = !(skip0 && mt == 0) &&
+                     (!(EIGENID_SP_SKIP && diag) ||
+                      (8 * (warp + kCW * mt) + 7 >= dskip &&
+                       row_ok(rb + 8 * (warp + kCW * mt) + 7, sn)));
         // ---- rank-2kB update of this lane's C rows
         double acc[kRW][kG2N / 8][2];
 #pragma unroll
-        for (int mt = 0; mt < kRW; ++mt)
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (skip0 && mt == 0) continue;
 #pragma unroll
           for (int nt = 0; nt < kG2N / 8; ++nt) {
             const double2 x = *reinterpret_cast<const double2*>(
@@ -1718,6 +1731,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
             acc[mt][nt][0] = x.x;
             acc[mt][nt][1] = x.y;
           }
+        }
 #pragma unroll
         for (int q = 0; q < kG2K / 8; ++q) {
           const int kl = (8 * q + 2 * kk) ^ (8 * (mm & 1));
@@ -1742,11 +1756,13 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         }
         // updated C rows to shared memory, arrive, row product, then wait
 #pragma unroll
-        for (int mt = 0; mt < kRW; ++mt)
+        for (int mt = 0; mt < kRW; ++mt) {
+          if (skip0 && mt == 0) continue;
 #pragma unroll
           for (int nt = 0; nt < kG2N / 8; ++nt)
             *reinterpret_cast<double2*>(cs + cswz(crow[mt], 8 * nt + 2 * kk)) =
                 make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(cbar);
         // ---- X[rb] += tril(C) VTn[cb] straight from the accumulators
@@ -1780,6 +1796,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #endif
 #pragma unroll
           for (int mt = 0; mt < kRW; ++mt) {
+            if (skip0 && mt == 0) continue;
             double* p = A22n + (long long)(rb + crow[mt]) * ldw + cb + 2 * kk;
 #pragma unroll
             for (int nt = 0; nt < kG2N / 8; ++nt)
@@ -1789,6 +1806,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         } else {
 #pragma unroll
           for (int mt = 0; mt < kRW; ++mt) {
+            if (skip0 && mt == 0) continue;
             const int r = rb + crow[mt];
 #pragma unroll
             for (int nt = 0; nt < kG2N / 8; ++nt) {
@@ -1813,7 +1831,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
         {
           const int ccol = 8 * mt2 + mm;
 #pragma unroll 4
-          for (int k4 = dskip / 4; k4 < kend4; ++k4) {
+          for (int k4 = skip0 ? kG2M / 8 : dskip / 4; k4 < kend4; ++k4) {
             const int krow = 4 * k4 + kk;
             const double v = cs[cswz(krow, ccol)];
             const double a = (diag && rb + krow <= cb + ccol) ? 0.0 : v;
@@ -1845,10 +1863,12 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       for (int ci = 0; ci < ncb; ++ci) {
         // EIGENID_SP_SKIP: 1 = diagonal and tail tiles, 2 = diagonal tiles
         // only, 3 = tail row blocks only (timing experiments)
-        if (ci * kG2N + kB > rb || ((EIGENID_SP_SKIP & 1) && !interior))
-          tile(ci, std::true_type{});
+        if (EIGENID_SP_SKIP0 && ci * kG2N - rb >= kG2M / 2)
+          tile(ci, std::true_type{}, std::true_type{});
+        else if (ci * kG2N + kB > rb || ((EIGENID_SP_SKIP & 1) && !interior))
+          tile(ci, std::true_type{}, std::false_type{});
         else
-          tile(ci, std::false_type{});
+          tile(ci, std::false_type{}, std::false_type{});
       }
       // the copy warps may now overwrite VTn[rb]
       __syncwarp();
