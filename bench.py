@@ -661,10 +661,10 @@ def our_config(args, dist: Dist, eng, wl: str, steps: int, warmup: int,
         t1 = st["stage1"] / 1e3
         achieved = f_tri(n, rows) / t1 / 1e12
         # DRAM bytes per solve of the stage-1 kernel at n = 4096 from one ncu
-        # --set full capture (profiles/r02h_band_4096_widesp_raw_summary.csv:
-        # 0.9970 TB read + 0.6088 TB written over the 146 solves of the captured launch), scaled to this
+        # --set full capture (profiles/r02j_band_4096_widesp_raw_summary.csv:
+        # 1.0028 TB read + 0.5993 TB written over the 146 solves of the captured launch), scaled to this
         # launch's solve count
-        traffic = (0.997006e12 + 0.608839e12) / 146 * (rows + 1) if n == 4096 else None
+        traffic = (1.002844e12 + 0.599308e12) / 146 * (rows + 1) if n == 4096 else None
         line["roofline"] = {
             "bound": "tensor", "kernel": "band_reduce_kernel (stage 1, dense->band, DMMA; widesp layout)",
             "achieved": achieved, "peak": P_FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
