@@ -992,6 +992,9 @@ __device__ __noinline__ void wait_timed_out(DevStatus* st, int site) {
 // Blocks until the barrier phase of the given parity has completed.  `site`
 // names the wait in the timeout report; once any wait of the call has timed
 // out, the others return at once so that the kernel unwinds.
+// kSleepNs > 0: back off between polls (a try_wait that fails returns after
+// ~100 cycles, so a waiting copy warp polls ~15 M times per second).
+template <int kSleepNs = 0>
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity,
                                           DevStatus* st, int site) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
@@ -1004,6 +1007,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+    if (kSleepNs > 0 && !done) __nanosleep(kSleepNs);
     if (!done && ((++spins) & 0xffu) == 0) {
       if (*(volatile const int*)&st->code == kWaitTimeoutCode) return;
       const long long now = clock64();
@@ -1477,6 +1481,11 @@ __device__ int g_drop_once = 1;
 #ifndef EIGENID_SP_SKIP0
 #define EIGENID_SP_SKIP0 1
 #endif
+// back-off of the copy warps' polls: measured 1 % SLOWER at 100 / 300 / 1000 ns
+// (the copies of tile g+2 go out later), so they poll without sleeping
+#ifndef EIGENID_SP_COPY_SLEEP_NS
+#define EIGENID_SP_COPY_SLEEP_NS 0
+#endif
 #ifndef EIGENID_SP_SKIP
 #define EIGENID_SP_SKIP 0
 #endif
@@ -1533,7 +1542,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
       for (int ci = 0; ci < ncb; ++ci, ++g) {
         const int sb = g % kFS;
         if (g >= kFS) {
-          mbar_wait(emptyb + sb, (ebits >> sb) & 1u, status, 4);
+          mbar_wait<EIGENID_SP_COPY_SLEEP_NS>(emptyb + sb, (ebits >> sb) & 1u, status, 4);
           ebits ^= 1u << sb;
         }
         double* st = sm + sb * kFSt;
@@ -1603,7 +1612,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           // VTn[rb] rows: the compute warps must be done with the previous
           // row block's transposed products
           if (rb != fused_rb0(sn)) {
-            mbar_wait(rbdone, rbpar, status, 5);
+            mbar_wait<EIGENID_SP_COPY_SLEEP_NS>(rbdone, rbpar, status, 5);
             rbpar ^= 1u;
           }
           for (int t = pt; t < kG2M * (kB / 2); t += kPT) {
