@@ -1483,6 +1483,10 @@ __device__ int g_drop_once = 1;
 #endif
 // back-off of the copy warps' polls: measured 1 % SLOWER at 100 / 300 / 1000 ns
 // (the copies of tile g+2 go out later), so they poll without sleeping
+// order of a tile's copies: the C tile (DRAM) before the Bop rows (mostly L2)
+#ifndef EIGENID_SP_C_FIRST
+#define EIGENID_SP_C_FIRST 0
+#endif
 #ifndef EIGENID_SP_COPY_SLEEP_NS
 #define EIGENID_SP_COPY_SLEEP_NS 0
 #endif
@@ -1558,6 +1562,21 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
           constexpr int kVIt = kB * (kB / 2) / kPT;
           static_assert(kBopRows % 2 == 0 && kCRows % 4 == 0, "swizzle terms must not change");
           const long long off = (long long)cb * kB;
+#if EIGENID_SP_C_FIRST
+          const int crw = pt >> 4, cc2 = (pt & 15) * 2;
+          const double* csrc = A22n + (long long)(rb + crw) * ldw + cb + cc2;
+          double* cdst = st + kG2N * kG2K + cswz(crw, cc2);
+#pragma unroll
+          for (int i = 0; i < kCIt; ++i)
+            cp_async16_full(cdst + i * kCRows * kG2N, csrc + (long long)i * kCRows * ldw);
+          const int brow = pt >> 5, bk2 = (pt & 31) * 2;
+          const double* bsrc =
+              (bk2 < kB ? Vp + bk2 : W2p + (bk2 - kB)) + off + (long long)brow * kB;
+          double* bdst = st + brow * kG2K + (bk2 ^ (8 * (brow & 1)));
+#pragma unroll
+          for (int i = 0; i < kBopIt; ++i)
+            cp_async16_full(bdst + i * kBopRows * kG2K, bsrc + i * kBopRows * kB);
+#else
           const int brow = pt >> 5, bk2 = (pt & 31) * 2;
           const double* bsrc =
               (bk2 < kB ? Vp + bk2 : W2p + (bk2 - kB)) + off + (long long)brow * kB;
@@ -1571,6 +1590,7 @@ __device__ void gemm_fused(double* A22n, int ldw, int sn, const double* W2p,
 #pragma unroll
           for (int i = 0; i < kCIt; ++i)
             cp_async16_full(cdst + i * kCRows * kG2N, csrc + (long long)i * kCRows * ldw);
+#endif
           const double* vsrc = VTn + off + (long long)crw * kB + cc2;
           double* vdst = st + kG2N * kG2K + kG2M * kG2N + crw * kFVLD + cc2;
 #pragma unroll
